@@ -1,0 +1,202 @@
+/*
+ * tri.h -- C ABI of libtri.so, the B200 (sm_100a) block-space triangular map
+ * lambda(omega) of Navarro, Bustos & Hitschfeld, "A Non-linear GPU Thread Map
+ * for Triangular Domains" (arXiv:1609.01490), and the kernels it drives.
+ *
+ * Citations: "P:a-b" = PAPER.md lines a-b (section / equation / table).
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only.  Pointers named d_* are DEVICE pointers (caller-owned,
+ *    e.g. torch tensors); h_* are host pointers.  The library allocates no
+ *    device memory, keeps no global state except a per-device SM-count cache,
+ *    and never synchronizes: every kernel call is enqueued asynchronously on
+ *    `stream` (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Argument validation is synchronous and returns a tri_status before any
+ *    launch; a launch failure is reported as TRI_ECUDA (cudaGetLastError);
+ *    kernel faults surface at the caller's next synchronization.
+ *  - Every output buffer comes with its capacity in bytes; a capacity smaller
+ *    than what the call writes returns TRI_EINVAL before any launch.
+ *  - Indices: cells (i, j) of the lower triangle 0 <= j <= i < n (P:86-87,
+ *    P:189-199).  The PACKED layout of Eq. 1 stores cell (i, j) at T(i) + j,
+ *    T(i) = i(i+1)/2; a rank's slice stores it at T(i) + j - out_offset.
+ *  - Strategies (every kernel has all three, P:411-418 for BB):
+ *      TRI_LAMBDA          one CTA per tile omega, 1-D grid of B tiles, tile
+ *                          coordinate = lambda(omega) (Eq. 4);
+ *      TRI_BB              m x m grid, tiles above the diagonal exit on a
+ *                          block test, diagonal tiles filter per thread;
+ *      TRI_LAMBDA_PERSIST  a grid of (SMs x resident CTAs) CTAs walking omega
+ *                          with a stride, lambda per tile (the B200 form).
+ */
+#ifndef TRI_H_
+#define TRI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TRI_OK = 0,
+    TRI_EINVAL = -1,  /* bad argument, NULL pointer, unsupported rho, buffer too small */
+    TRI_ERANGE = -2,  /* 64-bit capacity or the 2^40 omega bound exceeded              */
+    TRI_ECUDA = -3,   /* CUDA launch / runtime error                                   */
+    TRI_ENOTSUP = -4  /* valid request this build does not implement                   */
+} tri_status;
+
+enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2 };
+enum { TRI_DUMMY_FIXED = 0, TRI_DUMMY_PACKED = 1, TRI_DUMMY_DIGEST = 2, TRI_DUMMY_COUNT = 3 };
+
+/* Exactness bound of the device lambda: omega < 2^40 (checked exhaustively). */
+#define TRI_OMEGA_MAX (1ull << 40)
+
+/*
+ * Triangular-domain map descriptor.  Filled by tri_map_init; read-only
+ * afterwards; may be copied freely.
+ *   n            linear size of the domain (rows), n >= 1
+ *   rho          tile edge in cells ("dimensional block size")
+ *   diag         1: cells j <= i (D = n(n+1)/2); 0: strict j < i (D = n(n-1)/2)
+ *   rank, world  this process's share of a world-way partition (one GPU each)
+ *   m            ceil(n / rho) tiles per dimension
+ *   blocks       B = T(m) = m(m+1)/2 lambda tiles (Eq. 1)
+ *   cells        D (whole domain)
+ *   omega_begin, omega_end   this rank's lambda tile range [begin, end)
+ *   row_begin, row_end       this rank's cell rows [begin, end) (snapped to tile rows)
+ *   out_offset, out_cells    packed slice [T(row_begin), T(row_end)) of Eq. 1
+ *   waste_lambda, waste_bb   closed-form unnecessary threads of a whole-domain
+ *                            launch with one thread per cell: B rho^2 - D and
+ *                            m^2 rho^2 - D
+ *   snap         1: omega range = [T(R_g), T(R_g+1)), R_g the tile row minimising
+ *                |T(R) - g B / world| (lambda applied at partition level);
+ *                0: omega range = [floor(g B / world), floor((g+1) B / world))
+ */
+typedef struct {
+    int64_t n;
+    int32_t rho, diag, rank, world;
+    int64_t m;
+    uint64_t blocks, cells;
+    uint64_t omega_begin, omega_end;
+    int64_t row_begin, row_end;
+    uint64_t out_offset, out_cells;
+    uint64_t waste_lambda, waste_bb;
+    int32_t snap, reserved;
+} tri_map_t;
+
+/* P:180-205.  EINVAL: n < 1, rho < 1 or > 1024, world < 1, rank outside
+ * [0, world); ERANGE: T(m) >= 2^40 or T(n) overflows. */
+tri_status tri_map_init(tri_map_t *map, int64_t n, int32_t rho, int32_t diag,
+                        int32_t rank, int32_t world, int32_t snap_rows);
+
+/* Host mirror of the device map, Eq. 4 with the integer
+ * correction of the row-boundary property Eq. 3:
+ * (bi, bj) = (largest i with T(i) <= omega, omega - T(i)).  ERANGE: omega >= 2^40. */
+tri_status tri_lambda(uint64_t omega, uint32_t *bi, uint32_t *bj);
+
+/* GPU self-check of the map on omega in [omega0, omega0 + count):
+ * counts on device (into *d_fail, u64, zeroed by the call) every omega whose
+ * lambda violates Eq. 3 (T(i) <= omega < T(i+1)) or the Eq. 1 successor rule
+ * lambda(omega+1) in {(i, j+1), (i+1, 0)}.  If d_ij != NULL also writes
+ * d_ij[2t] = i, d_ij[2t+1] = j for t < count (requires count < 2^31).
+ * ERANGE: omega0 + count > 2^40. */
+tri_status tri_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ij,
+                        unsigned long long *d_fail, void *stream);
+
+/* Dummy kernel: each useful thread maps itself to (i,j).
+ *   FIXED  : writes i + j to d_out[0] (u32; racy by design)
+ *   PACKED : d_out[T(i)+j - out_offset] = (i<<16)|j as u32 when n <= 65536, else
+ *            (i<<32)|j as u64; needs out_cells * elem bytes.  Requires diag = 1.
+ *   DIGEST : *(u64*)d_out = sum over this rank's cells of (i + j) (zeroed by call)
+ *   COUNT  : 5 x u64 (zeroed by call): tiles dispatched, tiles discarded whole,
+ *            threads dispatched, useful threads, discarded threads.
+ * One thread per cell, rho x rho threads per CTA: rho in {8, 16, 32}. */
+tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode,
+                     void *d_out, size_t out_bytes, void *stream);
+
+/* Euclidean distance matrix: for this rank's packed slice,
+ * d_out[T(i)+j - out_offset] = || p_i - p_j ||_2 in fp32 for j <= i (diag = 1).
+ * d_pts: n points, point t at d_pts[t*ld .. t*ld+dim), dim in 1..4, ld >= dim.
+ * Requires out_bytes >= 4 * out_cells, d_out 16-byte aligned; rho in {32,64,128}.
+ * Stores are aligned 16-byte streaming stores; each 16-byte chunk of the slice
+ * is written by exactly one thread. */
+tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts,
+                   int32_t dim, int64_t ld, float *d_out, size_t out_bytes, void *stream);
+
+/* Host-buffer EDM (end-to-end through the ABI): h_pts/h_out are HOST buffers
+ * (pinned for overlap).  The packed output is produced in row bands of
+ * ~band_cells cells into the caller's device workspace d_ws (ws_bytes >=
+ * 2 * 4 * (band_cells + 4 * n)), and each band is copied to h_out while the
+ * next one is computed (two CUDA streams created and destroyed by the call).
+ * Synchronous: returns when h_out is complete.  d_pts_ws: device buffer of
+ * n*ld floats for the uploaded points. */
+tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_pts,
+                        int32_t dim, int64_t ld, float *d_pts_ws, float *h_out,
+                        size_t out_bytes, void *d_ws, size_t ws_bytes, uint64_t band_cells);
+
+/* Sphere collision count: *d_count (u64, zeroed by call) =
+ * number of pairs j < i in this rank's omega tiles with
+ *   d2 = fma(dz,dz, fma(dy,dy, dx*dx)) < (ri + rj)^2
+ * evaluated in IEEE fp32 round-to-nearest with exactly that operation order.
+ * d_spheres: n x 4 floats (x, y, z, r), 16-byte aligned.  rho in {64,128,256}.
+ * The map must be built with diag = 1 (tiles) -- the strict filter is per pair. */
+tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
+                       unsigned long long *d_count, void *stream);
+
+/* Device workspace tri_ca_step needs (bytes; may be 0). */
+size_t tri_ca_workspace_size(const tri_map_t *map);
+
+/* One synchronous generation of Life B3/S23 on the triangle (the
+ * rule is Conway's, cells outside the triangle dead).  d_in/d_out: this rank's
+ * packed slice (out_cells bytes, u8 {0,1}, 16-byte aligned, must not alias).
+ * d_halo_above = row row_begin-1 (row_begin bytes) or NULL (dead); d_halo_below
+ * = row row_end (row_end+1 bytes) or NULL (dead; ignored when row_end == n).
+ * rho (tile edge) in {128, 256, 512}.  d_ws: tri_ca_workspace_size bytes (NULL if 0). */
+tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_in,
+                       uint8_t *d_out, const uint8_t *d_halo_above,
+                       const uint8_t *d_halo_below, void *d_ws, void *stream);
+
+/*
+ * Tetrahedral map descriptor.  Tiles (i, j, k), j <= i <= k < m,
+ * enumerated layer-major (layer k = a triangle of side k+1, Eq. 1 inside).
+ *   blocks = T3(m) = m(m+1)(m+2)/6; rank's tile range [omega_begin, omega_end).
+ */
+typedef struct {
+    int64_t n;
+    int32_t rho, rank, world, reserved;
+    int64_t m;
+    uint64_t blocks, omega_begin, omega_end;
+    uint64_t waste_tet, waste_bb;  /* unnecessary threads (one per cell, strict p>q>s) */
+} tet_map_t;
+
+/* EINVAL: n < 3, rho not in {4, 8, 16}, bad rank/world. ERANGE: T3(m) >= 2^40. */
+tri_status tet_map_init(tet_map_t *map, int64_t n, int32_t rho, int32_t rank, int32_t world);
+
+/* Host mirror of the tetrahedral map (P:617-654 with integer correction):
+ * k = largest layer with T3(k) <= omega, (i, j) = lambda(omega - T3(k)). */
+tri_status tet_lambda(uint64_t omega, uint32_t *i, uint32_t *j, uint32_t *k);
+
+/* GPU self-check of the tetrahedral map on [omega0, omega0+count): failures of
+ * T3(k) <= omega < T3(k+1), j <= i <= k, and the layer-major successor rule. */
+tri_status tet_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ijk,
+                        unsigned long long *d_fail, void *stream);
+
+/* Triplet-interaction n-body on the tetrahedral map (
+ * interaction = Axilrod-Teller-Muto, reading Q15): for every
+ * triplet p > q > s in this rank's tiles, E = nu (1 + 3P/(8abc)) / (abc)^(3/2)
+ * with a = |x_p-x_q|^2, b = |x_q-x_s|^2, c = |x_s-x_p|^2,
+ * P = (a+c-b)(a+b-c)(b+c-a); d_energy[t] (n doubles, zeroed by the call) +=
+ * E/3 for t in {p, q, s}.  Terms in fp32, accumulation in fp64.
+ * d_pts4: n x 4 floats (x, y, z, unused), 16-byte aligned. */
+tri_status tet_triplet(const tet_map_t *map, int32_t strategy, const float *d_pts4,
+                       double nu, double *d_energy, void *stream);
+
+/* Number of kernels the most recent successful call on this host thread
+ * enqueued (for the bench's launch accounting). */
+int32_t tri_last_launch_count(void);
+
+const char *tri_status_str(tri_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRI_H_ */

@@ -63,6 +63,7 @@ def lib():
         L.orc_ca_run.argtypes = [i64, vp, i64]
         L.orc_ca_step_rows.argtypes = [i64, vp, vp, i64, i64]
         L.orc_triplet.argtypes = [i64, vp, ctypes.c_double, i64, i64, vp]
+        L.orc_triplet_abs.argtypes = [i64, vp, ctypes.c_double, i64, i64, vp]
         L.orc_triplet_total.argtypes = [i64, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
         L.orc_num_threads.restype = ctypes.c_int
         _lib = L
@@ -203,6 +204,15 @@ def triplet(pts4: np.ndarray, nu: float = 1.0, t_begin: int = 0, t_end: int | No
     e = np.zeros(max(t_end - t_begin, 1), np.float64)
     _check(lib().orc_triplet(n, _ptr(p), float(nu), t_begin, t_end, _ptr(e)))
     return e[: t_end - t_begin]
+
+
+def triplet_abs(pts4: np.ndarray, nu: float = 1.0, t_begin: int = 0, t_end: int | None = None) -> np.ndarray:
+    p = np.ascontiguousarray(pts4, np.float32)
+    n = p.shape[0]
+    t_end = n if t_end is None else t_end
+    a = np.zeros(max(t_end - t_begin, 1), np.float64)
+    _check(lib().orc_triplet_abs(n, _ptr(p), float(nu), t_begin, t_end, _ptr(a)))
+    return a[: t_end - t_begin]
 
 
 def triplet_total(pts4: np.ndarray, nu: float = 1.0) -> float:

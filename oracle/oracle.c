@@ -381,6 +381,26 @@ int orc_triplet(int64_t n, const float *pts, double nu, int64_t t_begin, int64_t
     return ORC_OK;
 }
 
+/* Per-particle absolute scale A_t = (1/3) sum |E| over the triplets containing t
+ * (the normaliser of the triplet tolerance, reading Q15); same loops as above. */
+int orc_triplet_abs(int64_t n, const float *pts, double nu, int64_t t_begin, int64_t t_end, double *a)
+{
+    if (n < 0 || t_begin < 0 || t_end > n || t_begin > t_end) return ORC_EINVAL;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t t = t_begin; t < t_end; ++t) {
+        double acc = 0.0;
+        for (int64_t u = 0; u < n; ++u) {
+            if (u == t) continue;
+            for (int64_t v = 0; v < u; ++v) {
+                if (v == t) continue;
+                acc += fabs(atm_energy(pts, t, u, v, nu));
+            }
+        }
+        a[t - t_begin] = acc / 3.0;
+    }
+    return ORC_OK;
+}
+
 /* Total energy sum_{p>q>s} E (the same definition, summed once per triplet). */
 int orc_triplet_total(int64_t n, const float *pts, double nu, double *total)
 {

@@ -1,0 +1,235 @@
+// abi.cu -- the C ABI of libtri.so (include/tri.h): descriptors, partition
+// arithmetic, validation and dispatch to the kernel launchers.
+#include <cstring>
+#include "tri_common.cuh"
+
+namespace tri {
+
+static thread_local int g_launches = 0;
+void note_launches(int k) { g_launches += k; }
+void reset_launches() { g_launches = 0; }
+
+int sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+// |world * T(r) - g * B| as unsigned 128-bit (partition snapping, reading Q17)
+static unsigned __int128 snap_dist(uint64_t r, uint64_t g, uint64_t B, uint64_t world) {
+    unsigned __int128 a = (unsigned __int128)world * T2(r);
+    unsigned __int128 b = (unsigned __int128)g * B;
+    return a > b ? a - b : b - a;
+}
+
+// Tile row R_g minimising |T(R) - g B / world|; ties -> the smaller row.
+static uint64_t snap_row(uint64_t g, uint64_t world, uint64_t m, uint64_t B) {
+    if (g == 0) return 0;
+    if (g >= world) return m;
+    uint64_t target = (uint64_t)(((unsigned __int128)g * B) / world);
+    uint32_t r, c;
+    lambda_map(target, r, c);        // lambda applied at partition level
+    uint64_t best = r;
+    if (r + 1 <= m && snap_dist(r + 1, g, B, world) < snap_dist(r, g, B, world)) best = r + 1;
+    return best > m ? m : best;
+}
+
+}  // namespace tri
+
+using namespace tri;
+
+extern "C" {
+
+tri_status tri_map_init(tri_map_t *map, int64_t n, int32_t rho, int32_t diag, int32_t rank,
+                        int32_t world, int32_t snap_rows) {
+    if (!map || n < 1 || rho < 1 || rho > 1024 || world < 1 || rank < 0 || rank >= world)
+        return TRI_EINVAL;
+    if (n > (int64_t)(1ll << 31)) return TRI_ERANGE;
+    tri_map_t t;
+    std::memset(&t, 0, sizeof t);
+    t.n = n; t.rho = rho; t.diag = diag ? 1 : 0; t.rank = rank; t.world = world;
+    t.snap = snap_rows ? 1 : 0;
+    t.m = (n + rho - 1) / rho;
+    const uint64_t m = (uint64_t)t.m;
+    t.blocks = T2(m);
+    if (t.blocks >= TRI_OMEGA_MAX) return TRI_ERANGE;
+    t.cells = t.diag ? T2((uint64_t)n) : T2((uint64_t)n - 1);
+    const uint64_t R0 = snap_row((uint64_t)rank, (uint64_t)world, m, t.blocks);
+    const uint64_t R1 = snap_row((uint64_t)rank + 1, (uint64_t)world, m, t.blocks);
+    t.row_begin = (int64_t)(R0 * (uint64_t)rho);
+    t.row_end = (int64_t)(R1 * (uint64_t)rho);
+    if (t.row_begin > n) t.row_begin = n;
+    if (t.row_end > n) t.row_end = n;
+    if (t.snap) {
+        t.omega_begin = T2(R0);
+        t.omega_end = T2(R1);
+    } else {
+        t.omega_begin = (uint64_t)(((unsigned __int128)rank * t.blocks) / (uint64_t)world);
+        t.omega_end = (uint64_t)(((unsigned __int128)(rank + 1) * t.blocks) / (uint64_t)world);
+    }
+    t.out_offset = T2((uint64_t)t.row_begin);
+    t.out_cells = T2((uint64_t)t.row_end) - t.out_offset;
+    const uint64_t r2 = (uint64_t)rho * (uint64_t)rho;
+    t.waste_lambda = t.blocks * r2 - t.cells;
+    t.waste_bb = m * m * r2 - t.cells;
+    *map = t;
+    return TRI_OK;
+}
+
+tri_status tri_lambda(uint64_t omega, uint32_t *bi, uint32_t *bj) {
+    if (!bi || !bj) return TRI_EINVAL;
+    if (omega >= TRI_OMEGA_MAX) return TRI_ERANGE;
+    lambda_map(omega, *bi, *bj);
+    return TRI_OK;
+}
+
+tri_status tri_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ij, unsigned long long *d_fail,
+                        void *stream) {
+    g_launches = 0;
+    if (!d_fail) return TRI_EINVAL;
+    if (omega0 > TRI_OMEGA_MAX || count > TRI_OMEGA_MAX - omega0) return TRI_ERANGE;
+    if (d_ij && count >= (1ull << 31)) return TRI_EINVAL;
+    return launch_map_eval(omega0, count, d_ij, d_fail, (cudaStream_t)stream);
+}
+
+static bool bad_strategy(int32_t s) { return s != TRI_LAMBDA && s != TRI_BB && s != TRI_LAMBDA_PERSIST; }
+
+static bool bad_map(const tri_map_t *m) {
+    return !m || m->n < 1 || m->rho < 1 || m->m != (m->n + m->rho - 1) / m->rho ||
+           m->blocks != T2((uint64_t)m->m) || m->omega_end < m->omega_begin ||
+           m->omega_end > m->blocks || m->row_begin < 0 || m->row_end > m->n ||
+           m->row_begin > m->row_end;
+}
+
+tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode, void *d_out,
+                     size_t out_bytes, void *stream) {
+    g_launches = 0;
+    if (bad_map(map) || bad_strategy(strategy) || !d_out) return TRI_EINVAL;
+    if (map->rho != 8 && map->rho != 16 && map->rho != 32) return TRI_EINVAL;
+    size_t need = 0;
+    switch (mode) {
+        case TRI_DUMMY_FIXED: need = 4; break;
+        case TRI_DUMMY_PACKED:
+            if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
+            need = map->out_cells * (map->n <= 65536 ? 4u : 8u);
+            break;
+        case TRI_DUMMY_DIGEST: need = 8; break;
+        case TRI_DUMMY_COUNT: need = 5 * 8; break;
+        default: return TRI_EINVAL;
+    }
+    if (out_bytes < need) return TRI_EINVAL;
+    return launch_dummy(*map, strategy, mode, d_out, (cudaStream_t)stream);
+}
+
+tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, int32_t dim, int64_t ld,
+                   float *d_out, size_t out_bytes, void *stream) {
+    g_launches = 0;
+    if (bad_map(map) || bad_strategy(strategy) || !d_pts || !d_out) return TRI_EINVAL;
+    if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
+    if (map->rho != 32 && map->rho != 64 && map->rho != 128) return TRI_EINVAL;
+    if (dim < 1 || dim > 4 || ld < dim) return TRI_EINVAL;
+    if (((uintptr_t)d_out & 15u) != 0) return TRI_EINVAL;
+    if (out_bytes < map->out_cells * 4u) return TRI_EINVAL;
+    if (map->out_cells == 0) return TRI_OK;
+    return launch_edm(*map, strategy, d_pts, dim, ld, d_out, (cudaStream_t)stream);
+}
+
+tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
+                       unsigned long long *d_count, void *stream) {
+    g_launches = 0;
+    if (bad_map(map) || bad_strategy(strategy) || !d_spheres || !d_count) return TRI_EINVAL;
+    if (map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
+    if (((uintptr_t)d_spheres & 15u) != 0) return TRI_EINVAL;
+    return launch_collide(*map, strategy, d_spheres, d_count, (cudaStream_t)stream);
+}
+
+size_t tri_ca_workspace_size(const tri_map_t *map) {
+    (void)map;
+    return 0;
+}
+
+tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_in, uint8_t *d_out,
+                       const uint8_t *d_halo_above, const uint8_t *d_halo_below, void *d_ws,
+                       void *stream) {
+    g_launches = 0;
+    (void)d_ws;
+    if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
+    if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
+    if (map->rho != 128 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
+    if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
+    if (map->out_cells == 0) return TRI_OK;
+    return launch_ca(*map, strategy, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);
+}
+
+tri_status tet_map_init(tet_map_t *map, int64_t n, int32_t rho, int32_t rank, int32_t world) {
+    if (!map || n < 3 || (rho != 4 && rho != 8 && rho != 16) || world < 1 || rank < 0 ||
+        rank >= world)
+        return TRI_EINVAL;
+    if (n > (1ll << 22)) return TRI_ERANGE;
+    tet_map_t t;
+    std::memset(&t, 0, sizeof t);
+    t.n = n; t.rho = rho; t.rank = rank; t.world = world;
+    t.m = (n + rho - 1) / rho;
+    const uint64_t m = (uint64_t)t.m;
+    t.blocks = T3(m);
+    if (t.blocks >= TRI_OMEGA_MAX) return TRI_ERANGE;
+    t.omega_begin = (uint64_t)(((unsigned __int128)rank * t.blocks) / (uint64_t)world);
+    t.omega_end = (uint64_t)(((unsigned __int128)(rank + 1) * t.blocks) / (uint64_t)world);
+    const uint64_t r3 = (uint64_t)rho * rho * rho;
+    const uint64_t nn = (uint64_t)n;
+    const uint64_t useful = nn * (nn - 1) * (nn - 2) / 6;   // C(n,3): p > q > s
+    t.waste_tet = t.blocks * r3 - useful;
+    t.waste_bb = m * m * m * r3 - useful;
+    *map = t;
+    return TRI_OK;
+}
+
+tri_status tet_lambda(uint64_t omega, uint32_t *i, uint32_t *j, uint32_t *k) {
+    if (!i || !j || !k) return TRI_EINVAL;
+    if (omega >= TRI_OMEGA_MAX) return TRI_ERANGE;
+    tet_map(omega, *i, *j, *k);
+    return TRI_OK;
+}
+
+tri_status tet_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ijk, unsigned long long *d_fail,
+                        void *stream) {
+    g_launches = 0;
+    if (!d_fail) return TRI_EINVAL;
+    if (omega0 > TRI_OMEGA_MAX || count > TRI_OMEGA_MAX - omega0) return TRI_ERANGE;
+    if (d_ijk && count >= (1ull << 30)) return TRI_EINVAL;
+    return launch_tet_map_eval(omega0, count, d_ijk, d_fail, (cudaStream_t)stream);
+}
+
+tri_status tet_triplet(const tet_map_t *map, int32_t strategy, const float *d_pts4, double nu,
+                       double *d_energy, void *stream) {
+    g_launches = 0;
+    if (!map || bad_strategy(strategy) || !d_pts4 || !d_energy) return TRI_EINVAL;
+    if (map->n < 3 || map->m != (map->n + map->rho - 1) / map->rho || map->blocks != T3((uint64_t)map->m) ||
+        map->omega_end > map->blocks || map->omega_begin > map->omega_end)
+        return TRI_EINVAL;
+    if (((uintptr_t)d_pts4 & 15u) != 0) return TRI_EINVAL;
+    return launch_triplet(*map, strategy, d_pts4, nu, d_energy, (cudaStream_t)stream);
+}
+
+int32_t tri_last_launch_count(void) { return g_launches; }
+
+const char *tri_status_str(tri_status s) {
+    switch (s) {
+        case TRI_OK: return "TRI_OK";
+        case TRI_EINVAL: return "TRI_EINVAL: invalid argument";
+        case TRI_ERANGE: return "TRI_ERANGE: size exceeds the 64-bit / 2^40 bound";
+        case TRI_ECUDA: return "TRI_ECUDA: CUDA error";
+        case TRI_ENOTSUP: return "TRI_ENOTSUP: not supported";
+    }
+    return "unknown tri_status";
+}
+
+}  // extern "C"

@@ -1,0 +1,283 @@
+// edm.cu -- Euclidean distance matrix on the packed lower triangle
+// (readings Q7/Q8), HBM-write bound.
+//
+// Tile = rho x rho cells, tile coordinate from lambda(omega) (Eq. 4) or the BB
+// grid.  The packed Eq. 1 layout puts row i at T(i), so a tile's
+// row segment starts at an arbitrary 4-byte offset.  To issue only aligned
+// 16-byte streaming stores, every aligned 4-float CHUNK of the output slice is
+// owned by the tile that holds the chunk's first cell; the owner computes all
+// four cells even when they run past the tile edge (EDM is pointwise, so the
+// neighbour cells are computable anywhere).  Consequences:
+//   * rho/4 chunk lanes per row segment; at rho = 128 one warp covers one row
+//     segment with one 512-byte coalesced st.global.cs.v4 per row;
+//   * the row's chunk phase delta = (-T(i)) mod 4 is warp-uniform at rho = 128,
+//     so each lane picks its 4 columns from a 7-column register window with a
+//     uniform switch (no shuffles, no shared memory);
+//   * a chunk that crosses the end of row i (diagonal tile) or of the slice
+//     takes a scalar slow path (one per row end).
+// Column points are loaded once per tile per lane (7 x dim floats, L1/L2
+// resident: 786 KB for n = 65536), row points once per row (warp broadcast).
+#include "tri_common.cuh"
+
+namespace {
+
+struct EdmArgs {
+    const float *pts;
+    int64_t ld, n;
+    uint64_t omega_begin, omega_end;
+    int64_t tile_row_begin;
+    uint64_t out_offset, out_cells;
+    float *out;
+};
+
+constexpr int kEdmThreads = 256;
+
+template <int DIM>
+__device__ __forceinline__ float dist_reg(const float (&p)[DIM], const float (&w)[DIM][7], int t) {
+    float dx = p[0] - w[0][t];
+    float d2 = dx * dx;
+#pragma unroll
+    for (int d = 1; d < DIM; ++d) {
+        const float dd = p[d] - w[d][t];
+        d2 = fmaf(dd, dd, d2);
+    }
+    return sqrt_approx(d2);
+}
+
+template <int DIM>
+__device__ __forceinline__ float dist_gmem(const EdmArgs &a, int64_t i, int64_t j) {
+    float d2 = 0.f;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        const float dd = __ldg(a.pts + i * a.ld + d) - __ldg(a.pts + j * a.ld + d);
+        d2 = d == 0 ? dd * dd : fmaf(dd, dd, d2);
+    }
+    return sqrt_approx(d2);
+}
+
+template <int RHO, int DIM>
+__device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
+    constexpr int L = RHO / 4;                 // chunk lanes per row segment
+    constexpr int RPW = 32 / L;                // rows per warp pass
+    constexpr int NW = kEdmThreads / 32;
+    constexpr int ROWS_PER_WARP = RHO / NW;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = lane % L, rs = lane / L;
+    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
+
+    float w[DIM][7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+        const int64_t col = c0 + 4 * k + t;
+        const bool in = col < a.n;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) w[d][t] = in ? __ldg(a.pts + col * a.ld + d) : 0.f;
+    }
+
+    const int64_t rbase = r0 + (int64_t)warp * ROWS_PER_WARP;
+#pragma unroll 1
+    for (int rr = rs; rr < ROWS_PER_WARP; rr += RPW) {
+        const int64_t i = rbase + rr;
+        if (i >= a.n) break;
+        float p[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) p[d] = __ldg(a.pts + i * a.ld + d);
+        const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.out_offset;  // local segment start
+        const int64_t seg = i - c0 + 1;
+        const int64_t len = seg < RHO ? seg : RHO;
+        const int delta = (int)((0u - (uint32_t)s) & 3u);
+        const int off = delta + 4 * k;
+        if (off >= len) continue;                      // chunk owned by the next segment
+        const uint64_t c = s + (uint64_t)off;
+        float *dst = a.out + c;
+        if (c0 + off + 3 <= i && c + 4 <= a.out_cells) {
+            float v0, v1, v2, v3;
+            switch (delta) {
+                case 0: v0 = dist_reg<DIM>(p, w, 0); v1 = dist_reg<DIM>(p, w, 1);
+                        v2 = dist_reg<DIM>(p, w, 2); v3 = dist_reg<DIM>(p, w, 3); break;
+                case 1: v0 = dist_reg<DIM>(p, w, 1); v1 = dist_reg<DIM>(p, w, 2);
+                        v2 = dist_reg<DIM>(p, w, 3); v3 = dist_reg<DIM>(p, w, 4); break;
+                case 2: v0 = dist_reg<DIM>(p, w, 2); v1 = dist_reg<DIM>(p, w, 3);
+                        v2 = dist_reg<DIM>(p, w, 4); v3 = dist_reg<DIM>(p, w, 5); break;
+                default: v0 = dist_reg<DIM>(p, w, 3); v1 = dist_reg<DIM>(p, w, 4);
+                         v2 = dist_reg<DIM>(p, w, 5); v3 = dist_reg<DIM>(p, w, 6); break;
+            }
+            st_cs_v4(dst, v0, v1, v2, v3);
+        } else {
+            // chunk crosses the end of row i and/or of the slice: walk Eq. 1
+            float v[4];
+            int64_t ii = i, jj = c0 + off;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                while (jj > ii) { jj -= ii + 1; ++ii; }
+                v[q] = (c + q < a.out_cells && ii < a.n) ? dist_gmem<DIM>(a, ii, jj) : 0.f;
+                ++jj;
+            }
+            if (c + 4 <= a.out_cells) {
+                st_cs_v4(dst, v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (c + q < a.out_cells) dst[q] = v[q];
+            }
+        }
+    }
+}
+
+template <int RHO, int DIM, int STRAT>
+__global__ void __launch_bounds__(kEdmThreads) edm_kernel(EdmArgs a) {
+    if (STRAT == TRI_BB) {
+        const uint32_t bj = blockIdx.x;
+        const uint32_t bi = blockIdx.y + (uint32_t)a.tile_row_begin;
+        if (bj > bi) return;                                  // discard
+        edm_tile<RHO, DIM>(a, bi, bj);
+    } else if (STRAT == TRI_LAMBDA) {
+        const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (w >= a.omega_end) return;
+        uint32_t bi, bj;
+        tri::lambda_map(w, bi, bj);
+        edm_tile<RHO, DIM>(a, bi, bj);
+    } else {
+#pragma unroll 1
+        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
+            uint32_t bi, bj;
+            tri::lambda_map(w, bi, bj);
+            edm_tile<RHO, DIM>(a, bi, bj);
+        }
+    }
+}
+
+template <int RHO, int DIM>
+tri_status launch_rd(const tri_map_t &m, int strategy, EdmArgs a, cudaStream_t st) {
+    if (strategy == TRI_BB) {
+        const int64_t tr0 = m.row_begin / m.rho;
+        const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;
+        if (tr1 <= tr0) return TRI_OK;
+        if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
+        a.tile_row_begin = tr0;
+        edm_kernel<RHO, DIM, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), kEdmThreads, 0, st>>>(a);
+    } else if (strategy == TRI_LAMBDA) {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        edm_kernel<RHO, DIM, TRI_LAMBDA><<<tri::tile_grid(nb), kEdmThreads, 0, st>>>(a);
+    } else {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edm_kernel<RHO, DIM, TRI_LAMBDA_PERSIST>,
+                                                      kEdmThreads, 0);
+        uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
+        if (g > nb) g = nb;
+        edm_kernel<RHO, DIM, TRI_LAMBDA_PERSIST><<<(unsigned)g, kEdmThreads, 0, st>>>(a);
+    }
+    tri::note_launches(1);
+    return tri::cuda_status();
+}
+
+template <int RHO>
+tri_status launch_r(const tri_map_t &m, int strategy, int dim, EdmArgs a, cudaStream_t st) {
+    switch (dim) {
+        case 1: return launch_rd<RHO, 1>(m, strategy, a, st);
+        case 2: return launch_rd<RHO, 2>(m, strategy, a, st);
+        case 3: return launch_rd<RHO, 3>(m, strategy, a, st);
+        default: return launch_rd<RHO, 4>(m, strategy, a, st);
+    }
+}
+
+}  // namespace
+
+namespace tri {
+
+tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int dim, int64_t ld, float *out,
+                      cudaStream_t st) {
+    EdmArgs a;
+    a.pts = pts; a.ld = ld; a.n = m.n;
+    a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
+    a.tile_row_begin = 0;
+    a.out_offset = m.out_offset; a.out_cells = m.out_cells;
+    a.out = out;
+    switch (m.rho) {
+        case 32: return launch_r<32>(m, strategy, dim, a, st);
+        case 64: return launch_r<64>(m, strategy, dim, a, st);
+        default: return launch_r<128>(m, strategy, dim, a, st);
+    }
+}
+
+}  // namespace tri
+
+// ---------------------------------------------------------------- host-buffer EDM
+// Row bands (multiples of rho rows) are computed into a ping-pong device
+// workspace and copied to the host buffer while the next band computes.
+extern "C" tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_pts, int32_t dim,
+                                   int64_t ld, float *d_pts_ws, float *h_out, size_t out_bytes, void *d_ws,
+                                   size_t ws_bytes, uint64_t band_cells) {
+    using namespace tri;
+    reset_launches();
+    if (!map || !h_pts || !d_pts_ws || !h_out || !d_ws) return TRI_EINVAL;
+    if (!map->diag || map->rho < 1) return TRI_EINVAL;
+    if (out_bytes < map->out_cells * 4u || (((uintptr_t)d_ws) & 15u)) return TRI_EINVAL;
+    uint64_t cap = (ws_bytes / 2 / 4) & ~3ull;          // floats per buffer, 16-byte multiple
+    if (band_cells && band_cells < cap) cap = band_cells & ~3ull;
+    const int64_t rho = map->rho;
+    float *buf[2] = {(float *)d_ws, (float *)d_ws + ((ws_bytes / 2 / 4) & ~3ull)};
+    cudaStream_t sc = nullptr, sx = nullptr;
+    cudaEvent_t done_k[2] = {nullptr, nullptr}, done_c[2] = {nullptr, nullptr};
+    tri_status rc = TRI_OK;
+    int launches = 0;
+    if (cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking) != cudaSuccess) {
+        rc = TRI_ECUDA;
+    }
+    for (int b = 0; b < 2 && rc == TRI_OK; ++b)
+        if (cudaEventCreateWithFlags(&done_k[b], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&done_c[b], cudaEventDisableTiming) != cudaSuccess)
+            rc = TRI_ECUDA;
+    if (rc == TRI_OK &&
+        cudaMemcpyAsync(d_pts_ws, h_pts, (size_t)map->n * (size_t)ld * 4u, cudaMemcpyHostToDevice, sc) !=
+            cudaSuccess)
+        rc = TRI_ECUDA;
+    int64_t ra = map->row_begin;
+    int band = 0;
+    while (rc == TRI_OK && ra < map->row_end) {
+        int64_t rb = ra + rho;
+        if (rb > map->row_end) rb = map->row_end;
+        while (rb < map->row_end) {
+            int64_t nx = rb + rho > map->row_end ? map->row_end : rb + rho;
+            if (T2((uint64_t)nx) - T2((uint64_t)ra) > cap) break;
+            rb = nx;
+        }
+        const uint64_t cells = T2((uint64_t)rb) - T2((uint64_t)ra);
+        if (cells > cap) { rc = TRI_EINVAL; break; }
+        tri_map_t bm = *map;
+        bm.row_begin = ra; bm.row_end = rb;
+        bm.omega_begin = T2((uint64_t)(ra / rho));
+        bm.omega_end = T2((uint64_t)((rb + rho - 1) / rho));
+        bm.out_offset = T2((uint64_t)ra);
+        bm.out_cells = cells;
+        const int slot = band & 1;
+        if (band >= 2) cudaStreamWaitEvent(sc, done_c[slot], 0);
+        rc = launch_edm(bm, strategy, d_pts_ws, dim, ld, buf[slot], sc);
+        if (rc != TRI_OK) break;
+        ++launches;
+        cudaEventRecord(done_k[slot], sc);
+        cudaStreamWaitEvent(sx, done_k[slot], 0);
+        if (cudaMemcpyAsync(h_out + (bm.out_offset - map->out_offset), buf[slot], cells * 4u,
+                            cudaMemcpyDeviceToHost, sx) != cudaSuccess) {
+            rc = TRI_ECUDA;
+            break;
+        }
+        cudaEventRecord(done_c[slot], sx);
+        ra = rb;
+        ++band;
+    }
+    if (sc && cudaStreamSynchronize(sc) != cudaSuccess) rc = TRI_ECUDA;
+    if (sx && cudaStreamSynchronize(sx) != cudaSuccess) rc = TRI_ECUDA;
+    for (int b = 0; b < 2; ++b) {
+        if (done_k[b]) cudaEventDestroy(done_k[b]);
+        if (done_c[b]) cudaEventDestroy(done_c[b]);
+    }
+    if (sc) cudaStreamDestroy(sc);
+    if (sx) cudaStreamDestroy(sx);
+    (void)launches;
+    return rc;
+}

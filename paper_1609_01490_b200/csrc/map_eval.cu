@@ -1,0 +1,87 @@
+// map_eval.cu -- GPU self-check of the 2-D and tetrahedral maps.
+//
+// For every omega in [w0, w0+count) the kernel evaluates the production map
+// (tri::lambda_map / tri::tet_map, the exact functions the workload kernels
+// use) and counts violations of
+//   Eq. 3:        T(i) <= omega < T(i+1), j <= i
+//   Eq. 1 successor: lambda(omega+1) in {(i, j+1), (i+1, 0)}
+// and for the tetrahedron the layer property T3(k) <= omega < T3(k+1),
+// j <= i <= k, and the layer-major successor rule.  A persistent grid walks
+// the range with a stride; each lane carries its own omega (no shuffles), and
+// failure counts are reduced per warp before one atomic.
+#include "tri_common.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(256) map_eval_kernel(uint64_t w0, uint64_t count, uint32_t *ij,
+                                                       unsigned long long *fail) {
+    unsigned long long bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+        const uint64_t w = w0 + t;
+        uint32_t i, j;
+        tri::lambda_map(w, i, j);
+        const uint64_t Ti = tri::T2(i);
+        bool ok = (Ti <= w) && (w < Ti + i + 1) && (j <= i) && (Ti + j == w);
+        uint32_t i2, j2;
+        tri::lambda_map(w + 1, i2, j2);
+        ok = ok && ((i2 == i && j2 == j + 1) || (i2 == i + 1 && j2 == 0));
+        bad += ok ? 0 : 1;
+        if (ij) { ij[2 * t] = i; ij[2 * t + 1] = j; }
+    }
+    bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(fail, bad);
+}
+
+__global__ void __launch_bounds__(256) tet_eval_kernel(uint64_t w0, uint64_t count, uint32_t *ijk,
+                                                       unsigned long long *fail) {
+    unsigned long long bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+        const uint64_t w = w0 + t;
+        uint32_t i, j, k;
+        tri::tet_map(w, i, j, k);
+        const uint64_t Tk = tri::T3(k);
+        bool ok = (Tk <= w) && (w < tri::T3((uint64_t)k + 1)) && (j <= i) && (i <= k) &&
+                  (Tk + tri::T2(i) + j == w);
+        uint32_t i2, j2, k2;
+        tri::tet_map(w + 1, i2, j2, k2);
+        ok = ok && ((k2 == k && i2 == i && j2 == j + 1) || (k2 == k && i2 == i + 1 && j2 == 0) ||
+                    (k2 == k + 1 && i2 == 0 && j2 == 0));
+        bad += ok ? 0 : 1;
+        if (ijk) { ijk[3 * t] = i; ijk[3 * t + 1] = j; ijk[3 * t + 2] = k; }
+    }
+    bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(fail, bad);
+}
+
+unsigned eval_grid(uint64_t count) {
+    uint64_t want = (count + 255) / 256;
+    uint64_t cap = (uint64_t)tri::sm_count() * 8ull * 16ull;
+    if (want > cap) want = cap;
+    return (unsigned)(want ? want : 1);
+}
+
+}  // namespace
+
+namespace tri {
+
+tri_status launch_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ij, unsigned long long *d_fail,
+                           cudaStream_t st) {
+    if (cudaMemsetAsync(d_fail, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
+    if (count == 0) return TRI_OK;
+    map_eval_kernel<<<eval_grid(count), 256, 0, st>>>(w0, count, d_ij, d_fail);
+    note_launches(1);
+    return cuda_status();
+}
+
+tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk, unsigned long long *d_fail,
+                               cudaStream_t st) {
+    if (cudaMemsetAsync(d_fail, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
+    if (count == 0) return TRI_OK;
+    tet_eval_kernel<<<eval_grid(count), 256, 0, st>>>(w0, count, d_ijk, d_fail);
+    note_launches(1);
+    return cuda_status();
+}
+
+}  // namespace tri

@@ -1,0 +1,114 @@
+// tri_common.cuh -- device/host primitives of the block-space map (sm_100a).
+//
+// "P:a-b" = PAPER.md lines.  The map lambda(omega) of Eq. 4 is
+// evaluated from an fp32 MUFU reciprocal-sqrt estimate of sqrt(8 omega + 1)
+// (the lambda_R idea of P:363-370) followed by ONE exact uint64 correction
+// step each way against the row-boundary property Eq. 3, which
+// replaces the paper's epsilon = 1e-4 patch.  The
+// estimate is within +-1 row for every omega < 2^40 (verified exhaustively on
+// the GPU by tri_map_eval), so lambda is exact on that range.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/tri.h"
+
+#define TRI_HD __host__ __device__ __forceinline__
+
+namespace tri {
+
+TRI_HD uint64_t T2(uint64_t r) { return r * (r + 1) / 2; }
+TRI_HD uint64_t T3(uint64_t r) { return r * (r + 1) * (r + 2) / 6; }
+
+// fp32 estimate of sqrt(x): MUFU.RSQ on the device, libm on the host.
+TRI_HD float sqrt_est(float x) {
+#ifdef __CUDA_ARCH__
+    return x * rsqrtf(x);   // MUFU.RSQ + FMUL (lambda_R form)
+#else
+    return sqrtf(x);
+#endif
+}
+
+// lambda(omega) -> (bi, bj), Eq. 4 with the Eq. 3 integer correction.
+TRI_HD void lambda_map(uint64_t w, uint32_t &bi, uint32_t &bj) {
+    const float x = (float)(8ull * w + 1ull);
+    const float s = sqrt_est(x);
+    float e = (s - 1.0f) * 0.5f;
+    e = e > 0.0f ? e : 0.0f;
+    uint32_t i = (uint32_t)e;
+    uint64_t t = T2(i);
+    if (t > w) { t -= i; --i; }                      // T(i-1) = T(i) - i
+    else if (t + i + 1 <= w) { t += i + 1; ++i; }    // T(i+1) = T(i) + i + 1
+    bi = i;
+    bj = (uint32_t)(w - t);
+}
+
+// Tetrahedral map: k = largest layer with T3(k) <= omega from an
+// fp32 cube-root estimate of (6 omega) (the real root y = x + 1 of
+// y^3 - y = 6 omega, reading Q13) plus one integer correction
+// step each way; then (i, j) = lambda(omega - T3(k)).
+TRI_HD void tet_map(uint64_t w, uint32_t &i, uint32_t &j, uint32_t &k) {
+    const float c = cbrtf((float)(6ull * w));
+    float e = c - 1.0f;
+    e = e > 0.0f ? e : 0.0f;
+    uint32_t kk = (uint32_t)e;
+    uint64_t t = T3(kk);
+    if (t > w) { --kk; t = T3(kk); }
+    else if (T3(kk + 1) <= w) { ++kk; t = T3(kk); }
+    k = kk;
+    lambda_map(w - t, i, j);
+}
+
+}  // namespace tri
+
+// ------------------------------------------------------------------ device stores
+__device__ __forceinline__ void st_cs_v4(float *p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d) : "memory");
+}
+__device__ __forceinline__ void st_cs_v4u(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+                 "r"(d) : "memory");
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ------------------------------------------------------------------ internal launch API
+namespace tri {
+
+// Per-call launch bookkeeping (thread-local in abi.cu).
+void note_launches(int k);
+void reset_launches();
+int sm_count();                       // SMs of the current device (cached)
+inline tri_status cuda_status() {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TRI_OK : TRI_ECUDA;
+}
+
+// Grid helper for lambda launches: nb tiles as (gx, gy) with gx*gy >= nb.
+inline dim3 tile_grid(uint64_t nb) {
+    const uint64_t gx_max = 1ull << 30;
+    uint64_t gx = nb < gx_max ? nb : gx_max;
+    if (gx == 0) gx = 1;
+    uint64_t gy = (nb + gx - 1) / gx;
+    return dim3((unsigned)gx, (unsigned)(gy ? gy : 1), 1);
+}
+
+// Kernel launchers (one per .cu file); args validated by abi.cu.
+tri_status launch_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ij, unsigned long long *d_fail,
+                           cudaStream_t st);
+tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk,
+                               unsigned long long *d_fail, cudaStream_t st);
+tri_status launch_dummy(const tri_map_t &m, int strategy, int mode, void *d_out, cudaStream_t st);
+tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int dim, int64_t ld,
+                      float *out, cudaStream_t st);
+tri_status launch_collide(const tri_map_t &m, int strategy, const float *sph,
+                          unsigned long long *count, cudaStream_t st);
+tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_t *out,
+                     const uint8_t *above, const uint8_t *below, cudaStream_t st);
+tri_status launch_triplet(const tet_map_t &m, int strategy, const float *pts, double nu,
+                          double *energy, cudaStream_t st);
+
+}  // namespace tri

@@ -1,0 +1,200 @@
+"""Thin ctypes binding of libtri.so (include/tri.h) -- argument marshalling only.
+
+Every function here has the C name and forwards to the library; tensors are
+passed as raw device pointers (``tensor.data_ptr()``) with their byte
+capacity, and the stream defaults to torch's current CUDA stream.  There is no
+compute in Python and no CPU fallback: if libtri.so cannot be loaded the first
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtri.so")
+
+TRI_OK, TRI_EINVAL, TRI_ERANGE, TRI_ECUDA, TRI_ENOTSUP = 0, -1, -2, -3, -4
+TRI_LAMBDA, TRI_BB, TRI_LAMBDA_PERSIST = 0, 1, 2
+TRI_DUMMY_FIXED, TRI_DUMMY_PACKED, TRI_DUMMY_DIGEST, TRI_DUMMY_COUNT = 0, 1, 2, 3
+STRATEGIES = {"lambda": TRI_LAMBDA, "bb": TRI_BB, "persist": TRI_LAMBDA_PERSIST}
+
+c_u64, c_i64, c_i32, c_u32, c_vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p
+
+
+class TriMap(ctypes.Structure):
+    """tri_map_t (include/tri.h)."""
+    _fields_ = [("n", c_i64), ("rho", c_i32), ("diag", c_i32), ("rank", c_i32), ("world", c_i32),
+                ("m", c_i64), ("blocks", c_u64), ("cells", c_u64),
+                ("omega_begin", c_u64), ("omega_end", c_u64),
+                ("row_begin", c_i64), ("row_end", c_i64),
+                ("out_offset", c_u64), ("out_cells", c_u64),
+                ("waste_lambda", c_u64), ("waste_bb", c_u64),
+                ("snap", c_i32), ("reserved", c_i32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
+class TetMap(ctypes.Structure):
+    """tet_map_t (include/tri.h)."""
+    _fields_ = [("n", c_i64), ("rho", c_i32), ("rank", c_i32), ("world", c_i32), ("reserved", c_i32),
+                ("m", c_i64), ("blocks", c_u64), ("omega_begin", c_u64), ("omega_end", c_u64),
+                ("waste_tet", c_u64), ("waste_bb", c_u64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
+class TriError(RuntimeError):
+    def __init__(self, code, what):
+        self.code = code
+        super().__init__(f"{what}: {status_str(code)} ({code})")
+
+
+_lib = None
+
+SIGNATURES = {
+    "tri_map_init": ([ctypes.POINTER(TriMap), c_i64, c_i32, c_i32, c_i32, c_i32, c_i32], c_i32),
+    "tri_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
+    "tri_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
+    "tri_dummy": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, ctypes.c_size_t, c_vp], c_i32),
+    "tri_edm": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp], c_i32),
+    "tri_edm_host": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_i32, c_i64, c_vp, c_vp, ctypes.c_size_t,
+                      c_vp, ctypes.c_size_t, c_u64], c_i32),
+    "tri_collide": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_vp, c_vp], c_i32),
+    "tri_ca_workspace_size": ([ctypes.POINTER(TriMap)], ctypes.c_size_t),
+    "tri_ca_step": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_i32),
+    "tet_map_init": ([ctypes.POINTER(TetMap), c_i64, c_i32, c_i32, c_i32], c_i32),
+    "tet_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
+    "tet_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
+    "tet_triplet": ([ctypes.POINTER(TetMap), c_i32, c_vp, ctypes.c_double, c_vp, c_vp], c_i32),
+    "tri_last_launch_count": ([], c_i32),
+    "tri_status_str": ([c_i32], ctypes.c_char_p),
+}
+
+
+def lib():
+    """Load libtri.so (raises if it is missing -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libtri.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (argt, rest) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = argt
+            fn.restype = rest
+        _lib = L
+    return _lib
+
+
+def status_str(code: int) -> str:
+    return lib().tri_status_str(code).decode()
+
+
+def _ok(code, what):
+    if code != TRI_OK:
+        raise TriError(code, what)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _nbytes(t):
+    return t.numel() * t.element_size()
+
+
+def _strategy(s):
+    return STRATEGIES[s] if isinstance(s, str) else int(s)
+
+
+# ----------------------------------------------------------------------------- map
+def tri_map_init(n, rho, diag=1, rank=0, world=1, snap_rows=1) -> TriMap:
+    m = TriMap()
+    _ok(lib().tri_map_init(ctypes.byref(m), n, rho, diag, rank, world, snap_rows), "tri_map_init")
+    return m
+
+
+def tri_lambda(omega):
+    bi, bj = c_u32(), c_u32()
+    _ok(lib().tri_lambda(omega, ctypes.byref(bi), ctypes.byref(bj)), "tri_lambda")
+    return bi.value, bj.value
+
+
+def tri_map_eval(omega0, count, d_ij, d_fail, stream=None):
+    _ok(lib().tri_map_eval(omega0, count, _ptr(d_ij), _ptr(d_fail), _stream(stream)), "tri_map_eval")
+
+
+def tet_map_init(n, rho, rank=0, world=1) -> TetMap:
+    m = TetMap()
+    _ok(lib().tet_map_init(ctypes.byref(m), n, rho, rank, world), "tet_map_init")
+    return m
+
+
+def tet_lambda(omega):
+    i, j, k = c_u32(), c_u32(), c_u32()
+    _ok(lib().tet_lambda(omega, ctypes.byref(i), ctypes.byref(j), ctypes.byref(k)), "tet_lambda")
+    return i.value, j.value, k.value
+
+
+def tet_map_eval(omega0, count, d_ijk, d_fail, stream=None):
+    _ok(lib().tet_map_eval(omega0, count, _ptr(d_ijk), _ptr(d_fail), _stream(stream)), "tet_map_eval")
+
+
+# ----------------------------------------------------------------------------- kernels
+def tri_dummy(m: TriMap, strategy, mode, out, stream=None):
+    _ok(lib().tri_dummy(ctypes.byref(m), _strategy(strategy), mode, _ptr(out), _nbytes(out), _stream(stream)),
+        "tri_dummy")
+
+
+def tri_edm(m: TriMap, strategy, pts, out, stream=None):
+    """pts: (n, dim) float32 CUDA tensor (row stride = pts.stride(0)); out: float32 >= out_cells."""
+    assert pts.dim() == 2 and pts.stride(1) == 1
+    _ok(lib().tri_edm(ctypes.byref(m), _strategy(strategy), _ptr(pts), pts.shape[1], pts.stride(0),
+                      _ptr(out), _nbytes(out), _stream(stream)), "tri_edm")
+
+
+def tri_edm_host(m: TriMap, strategy, h_pts, d_pts_ws, h_out, d_ws, band_cells=0):
+    """Host-buffer EDM (synchronous): h_pts/h_out CPU tensors (pinned for overlap)."""
+    assert h_pts.dim() == 2 and h_pts.stride(1) == 1
+    _ok(lib().tri_edm_host(ctypes.byref(m), _strategy(strategy), _ptr(h_pts), h_pts.shape[1], h_pts.stride(0),
+                           _ptr(d_pts_ws), _ptr(h_out), _nbytes(h_out), _ptr(d_ws), _nbytes(d_ws), band_cells),
+        "tri_edm_host")
+
+
+def tri_collide(m: TriMap, strategy, spheres, count, stream=None):
+    """spheres: (n, 4) float32 CUDA tensor (x, y, z, r); count: int64/uint64 CUDA tensor (>= 1 elem)."""
+    assert spheres.dim() == 2 and spheres.shape[1] == 4 and spheres.is_contiguous()
+    _ok(lib().tri_collide(ctypes.byref(m), _strategy(strategy), _ptr(spheres), _ptr(count), _stream(stream)),
+        "tri_collide")
+
+
+def tri_ca_workspace_size(m: TriMap) -> int:
+    return int(lib().tri_ca_workspace_size(ctypes.byref(m)))
+
+
+def tri_ca_step(m: TriMap, strategy, state_in, state_out, halo_above=None, halo_below=None, ws=None,
+                stream=None):
+    _ok(lib().tri_ca_step(ctypes.byref(m), _strategy(strategy), _ptr(state_in), _ptr(state_out),
+                          _ptr(halo_above), _ptr(halo_below), _ptr(ws), _stream(stream)), "tri_ca_step")
+
+
+def tet_triplet(m: TetMap, strategy, pts4, energy, nu=1.0, stream=None):
+    assert pts4.dim() == 2 and pts4.shape[1] == 4 and pts4.is_contiguous()
+    _ok(lib().tet_triplet(ctypes.byref(m), _strategy(strategy), _ptr(pts4), float(nu), _ptr(energy),
+                          _stream(stream)), "tet_triplet")
+
+
+def tri_last_launch_count() -> int:
+    return int(lib().tri_last_launch_count())

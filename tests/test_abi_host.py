@@ -1,0 +1,145 @@
+"""Host-side tests of the C ABI (-m "not gpu"): the library loads, exports every
+symbol include/tri.h declares, and its pure-host entry points (descriptor,
+partition, host mirror of lambda) agree with the oracle.  No kernel launches."""
+import math
+import os
+import random
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+tri = pytest.importorskip("paper_1609_01490_b200.tri")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1609_01490_b200 import build
+    build.build()
+    return tri.lib()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "tri.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b((?:tri|tet)_\w+)\s*\(", src, re.M)))
+
+
+def test_header_parses():
+    fns = header_functions()
+    for must in ("tri_map_init", "tri_dummy", "tri_edm", "tri_collide", "tri_ca_step", "tet_triplet"):
+        assert must in fns
+
+
+def test_library_exports_every_header_symbol(L):
+    out = subprocess.run(["nm", "-D", "--defined-only", tri.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT\s+(\w+)$", out, re.M))
+    missing = [f for f in header_functions() if f not in exported]
+    assert not missing, missing
+    for f in header_functions():
+        assert hasattr(L, f)
+    assert set(tri.SIGNATURES) == set(header_functions())
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", tri.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def T(r):
+    return r * (r + 1) // 2
+
+
+def test_status_strings(L):
+    assert tri.status_str(0) == "TRI_OK"
+    assert "EINVAL" in tri.status_str(-1)
+
+
+def test_map_init_single(L):
+    m = tri.tri_map_init(2048, 16)
+    assert (m.m, m.blocks, m.cells) == (128, 8256, 2098176)
+    assert (m.omega_begin, m.omega_end, m.row_begin, m.row_end) == (0, 8256, 0, 2048)
+    assert (m.out_offset, m.out_cells) == (0, 2098176)
+    assert m.waste_lambda == 15360 and m.waste_bb == 2096128
+    m = tri.tri_map_init(65536, 128)
+    assert m.blocks == 512 * 513 // 2 and m.cells == 2147516416
+
+
+@pytest.mark.parametrize("n,rho,world", [(65536, 16, 8), (65536, 128, 8), (1000, 32, 3), (37, 8, 4),
+                                         (200000, 256, 8), (100, 128, 2), (5, 128, 4)])
+def test_partition_snapped(L, n, rho, world):
+    maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+    m = -(-n // rho)
+    B = T(m)
+    # contiguous cover of [0, B) and of the packed slice [0, D)
+    assert maps[0].omega_begin == 0 and maps[-1].omega_end == B
+    assert maps[0].out_offset == 0 and maps[-1].out_offset + maps[-1].out_cells == T(n)
+    for a, b in zip(maps, maps[1:]):
+        assert a.omega_end == b.omega_begin and a.row_end == b.row_begin
+        assert a.out_offset + a.out_cells == b.out_offset
+    # snapped row R_g minimises |T(R) - g B / world|, ties to the smaller (reading Q17)
+    R = [min(range(m + 1), key=lambda r: (abs(world * T(r) - g * B), r)) for g in range(world + 1)]
+    for g, x in enumerate(maps):
+        assert x.omega_begin == T(R[g]) and x.omega_end == T(R[g + 1])
+        assert x.row_begin == min(R[g] * rho, n) and x.row_end == min(R[g + 1] * rho, n)
+    maps = [x for x in maps if x.row_begin // rho < m]
+    if n == 65536 and rho == 16 and world == 8:      # SURVEY §8a a1 (derived bounds)
+        assert [x.row_begin // rho for x in maps] + [m] == [0, 1448, 2048, 2508, 2896, 3238, 3547, 3831, 4096]
+
+
+@pytest.mark.parametrize("n,rho,world", [(200000, 256, 8), (1000, 64, 3), (10, 64, 4)])
+def test_partition_plain(L, n, rho, world):
+    maps = [tri.tri_map_init(n, rho, 1, g, world, 0) for g in range(world)]
+    B = T(-(-n // rho))
+    for g, x in enumerate(maps):
+        assert x.omega_begin == g * B // world and x.omega_end == (g + 1) * B // world
+
+
+def test_map_init_errors(L):
+    for args in [(0, 16), (10, 0), (10, 2000), (10, 16, 1, 2, 2), (10, 16, 1, -1, 2)]:
+        with pytest.raises(tri.TriError) as e:
+            tri.tri_map_init(*args)
+        assert e.value.code == tri.TRI_EINVAL
+    with pytest.raises(tri.TriError) as e:
+        tri.tri_map_init(2**31 + 1, 1)
+    assert e.value.code == tri.TRI_ERANGE
+
+
+def test_host_lambda_vs_oracle(L, orc):
+    rng = random.Random(5)
+    ws = list(range(0, 5000)) + [rng.randrange(0, 2**40) for _ in range(3000)]
+    for r in (4607, 4608, 2**20, 1482909, 1482910):
+        ws += [T(r) - 1, T(r), T(r) + 1]
+    for w in ws:
+        if w < 2**40:
+            assert tri.tri_lambda(w) == orc.lam(w)
+    with pytest.raises(tri.TriError):
+        tri.tri_lambda(2**40)
+
+
+def test_host_tet_lambda_vs_oracle(L, orc):
+    rng = random.Random(6)
+    ws = list(range(0, 3000)) + [rng.randrange(0, 2**40) for _ in range(2000)]
+    for k in (5, 35, 511, 512, 4096, 10000):
+        t3 = k * (k + 1) * (k + 2) // 6
+        ws += [t3 - 1, t3, t3 + 1]
+    for w in ws:
+        assert tri.tet_lambda(w) == orc.tet_lam(w)
+
+
+def test_tet_map_init(L):
+    t = tri.tet_map_init(4096, 8)
+    assert t.m == 512 and t.blocks == 512 * 513 * 514 // 6 == 22500864
+    useful = 4096 * 4095 * 4094 // 6
+    assert t.waste_tet == t.blocks * 512 - useful
+    assert abs((t.waste_bb + useful) / (t.blocks * 512) - 5.965) < 1e-3    # ~6x
+    t = tri.tet_map_init(4096, 16)
+    assert t.blocks == 256 * 257 * 258 // 6
+    parts = [tri.tet_map_init(4096, 16, g, 4) for g in range(4)]
+    assert parts[0].omega_begin == 0 and parts[-1].omega_end == t.blocks
+    for a, b in zip(parts, parts[1:]):
+        assert a.omega_end == b.omega_begin
+    with pytest.raises(tri.TriError):
+        tri.tet_map_init(4096, 5)

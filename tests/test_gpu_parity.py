@@ -1,0 +1,387 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI against the CPU
+oracle, element by element on the same seeded inputs.
+
+Bars: bit-exact for indices, maps, dummy codes/digests/
+counts, collision counts and CA states; EDM within 1e-5 relative (1e-6 absolute
+near zero); triplet energies within 1e-5 of the per-particle scale
+A_t = (1/3) sum |E| (reading Q15), total within 1e-5 of sum |E|.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1609_01490_b200 import inputs  # noqa: E402
+from paper_1609_01490_b200 import tri  # noqa: E402
+
+STRATS = ["lambda", "bb", "persist"]
+
+
+def T(r):
+    return r * (r + 1) // 2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    tri.lib()
+    return torch.device("cuda:0")
+
+
+def sync():
+    torch.cuda.synchronize()
+
+
+# ============================================================== map
+def test_map_matches_enumeration(orc):
+    m = 2000
+    I, J = orc.enumerate_tri(m)
+    cnt = len(I)
+    ij = torch.empty(2 * cnt, dtype=torch.int32, device="cuda")
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_map_eval(0, cnt, ij, fail)
+    sync()
+    got = ij.cpu().numpy().astype(np.uint32).reshape(-1, 2)
+    assert np.array_equal(got[:, 0], I) and np.array_equal(got[:, 1], J)
+    assert fail.item() == 0
+
+
+def test_map_exact_to_2_40_exhaustive():
+    """Eq. 3 + successor rule for EVERY omega < 2^40 (the exactness bound)."""
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    total = 0
+    step = 1 << 38
+    for w0 in range(0, 1 << 40, step):
+        cnt = min(step, (1 << 40) - 1 - w0)   # successor of the last omega must stay < 2^40
+        tri.tri_map_eval(w0, cnt, None, fail)
+        sync()
+        total += fail.item()
+    assert total == 0
+
+
+def test_map_boundaries_sampled(orc):
+    ws = []
+    for r in [1, 2, 3, 4607, 4608, 4609, 65535, 65536, 2**20, 1482908]:
+        ws += [T(r) - 1, T(r), T(r) + 1]
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ij = torch.empty(2, dtype=torch.int32, device="cuda")
+    for w in ws:
+        tri.tri_map_eval(w, 1, ij, fail)
+        sync()
+        assert tuple(ij.cpu().numpy().astype(np.uint32).tolist()) == orc.lam(w)
+
+
+def test_tet_map_matches_enumeration_and_exhaustive(orc):
+    I, J, K = orc.enumerate_tet(120)
+    cnt = len(I)
+    ijk = torch.empty(3 * cnt, dtype=torch.int32, device="cuda")
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tet_map_eval(0, cnt, ijk, fail)
+    sync()
+    got = ijk.cpu().numpy().astype(np.uint32).reshape(-1, 3)
+    assert np.array_equal(got[:, 0], I) and np.array_equal(got[:, 1], J) and np.array_equal(got[:, 2], K)
+    assert fail.item() == 0
+    total = 0
+    step = 1 << 34
+    for w0 in range(0, 1 << 36, step):
+        tri.tet_map_eval(w0, step, None, fail)
+        sync()
+        total += fail.item()
+    assert total == 0
+
+
+# ============================================================== dummy
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("n,rho", [(1, 8), (2, 16), (5, 8), (100, 16), (2048, 16), (1000, 32), (333, 8)])
+def test_dummy_packed_digest_count(orc, strategy, n, rho):
+    m = tri.tri_map_init(n, rho)
+    out = torch.full((m.out_cells,), -1, dtype=torch.int32, device="cuda")
+    tri.tri_dummy(m, strategy, tri.TRI_DUMMY_PACKED, out)
+    sync()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), orc.dummy_packed(n))
+    dig = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_dummy(m, strategy, tri.TRI_DUMMY_DIGEST, dig)
+    sync()
+    assert dig.item() == orc.dummy_digest(n) == (n - 1) * n * (n + 1) // 2
+    cnt = torch.zeros(5, dtype=torch.int64, device="cuda")
+    tri.tri_dummy(m, strategy, tri.TRI_DUMMY_COUNT, cnt)
+    sync()
+    c = cnt.cpu().tolist()
+    ref = orc.dispatch_count(n, rho, 1 if strategy == "bb" else 0)
+    assert c == [ref["blocks"], ref["blocks_discarded"], ref["threads"], ref["useful"], ref["discarded"]]
+    fx = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tri.tri_dummy(m, strategy, tri.TRI_DUMMY_FIXED, fx)
+    sync()
+    assert 0 <= fx.item() <= 2 * (n - 1)      # some in-domain i+j (racy by design, Q6)
+
+
+def test_dummy_wide_codes(orc):
+    n = 65600
+    m = tri.tri_map_init(n, 32, 1, 7, 8, 1)   # last rank's slice: u64 codes
+    out = torch.empty((m.out_cells,), dtype=torch.int64, device="cuda")
+    tri.tri_dummy(m, "lambda", tri.TRI_DUMMY_PACKED, out)
+    sync()
+    ref = orc.dummy_packed(n, m.row_begin, m.row_end, elem_bytes=8)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), ref)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_dummy_ranks_concatenate(orc, world):
+    n, rho = 777, 16
+    parts = []
+    for g in range(world):
+        m = tri.tri_map_init(n, rho, 1, g, world, 1)
+        out = torch.full((max(m.out_cells, 1),), -1, dtype=torch.int32, device="cuda")
+        tri.tri_dummy(m, "lambda", tri.TRI_DUMMY_PACKED, out)
+        sync()
+        parts.append(out.cpu().numpy()[: m.out_cells].view(np.uint32))
+    assert np.array_equal(np.concatenate(parts), orc.dummy_packed(n))
+
+
+# ============================================================== EDM
+def edm_close(got, ref):
+    err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    tol = np.maximum(1e-5 * np.abs(ref.astype(np.float64)), 1e-6)
+    bad = err > tol
+    assert not bad.any(), (int(bad.sum()), float(err.max()))
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("rho", [32, 64, 128])
+@pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (3, 7), (5, 42), (64, 7), (257, 42), (1000, 7), (4097, 42)])
+def test_edm_small(orc, strategy, rho, n, seed):
+    pts = inputs.points(n, 3, seed)
+    m = tri.tri_map_init(n, rho)
+    out = torch.full((m.out_cells + 8,), float("nan"), dtype=torch.float32, device="cuda")
+    tri.tri_edm(m, strategy, torch.from_numpy(pts).cuda(), out)
+    sync()
+    got = out.cpu().numpy()
+    assert np.isnan(got[m.out_cells:]).all()        # nothing written past the slice
+    edm_close(got[: m.out_cells], orc.edm(pts))
+
+
+@pytest.mark.parametrize("dim", [1, 2, 4])
+def test_edm_dims_and_stride(orc, dim):
+    n = 777
+    pts = inputs.points(n, dim, 7)
+    m = tri.tri_map_init(n, 128)
+    out = torch.empty((m.out_cells,), dtype=torch.float32, device="cuda")
+    wide = torch.zeros((n, 6), dtype=torch.float32)
+    wide[:, :dim] = torch.from_numpy(pts)
+    tri.tri_edm(m, "lambda", wide.cuda()[:, :dim], out)      # ld = 6 > dim
+    sync()
+    edm_close(out.cpu().numpy(), orc.edm(pts))
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_edm_ranks_concatenate(orc, world):
+    n = 3001
+    pts = inputs.points(n, 3, 42)
+    d = torch.from_numpy(pts).cuda()
+    parts = []
+    for g in range(world):
+        m = tri.tri_map_init(n, 64, 1, g, world, 1)
+        out = torch.empty((max(m.out_cells, 4),), dtype=torch.float32, device="cuda")
+        tri.tri_edm(m, "persist", d, out)
+        sync()
+        parts.append(out.cpu().numpy()[: m.out_cells])
+    edm_close(np.concatenate(parts), orc.edm(pts))
+
+
+def test_edm_full_size_sampled(orc):
+    """BASELINE configs[1]: n = 65536, 3-D, the bench's launch (rho 128, persistent)."""
+    n = 65536
+    pts = inputs.points(n, 3, 42)
+    m = tri.tri_map_init(n, 128)
+    out = torch.full((m.out_cells,), float("nan"), dtype=torch.float32, device="cuda")
+    tri.tri_edm(m, "persist", torch.from_numpy(pts).cuda(), out)
+    sync()
+    assert not torch.isnan(out).any().item()           # every cell written
+    for rb, re in [(0, 64), (20000, 20030), (40961, 40970), (65500, 65536)]:
+        got = out[T(rb):T(re)].cpu().numpy()
+        edm_close(got, orc.edm(pts, rb, re))
+    del out
+
+
+def test_edm_host_e2e(orc):
+    n = 5000
+    pts = torch.from_numpy(inputs.points(n, 3, 7))
+    m = tri.tri_map_init(n, 128)
+    h_out = torch.empty((m.out_cells,), dtype=torch.float32).pin_memory()
+    ws = torch.empty((2 * 4 * 1_000_000,), dtype=torch.uint8, device="cuda")
+    dp = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    tri.tri_edm_host(m, "persist", pts.pin_memory(), dp, h_out, ws, band_cells=1_000_000)
+    edm_close(h_out.numpy(), orc.edm(pts.numpy()))
+
+
+# ============================================================== collision
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("rho", [64, 128, 256])
+@pytest.mark.parametrize("n,seed,rmax", [(1, 7, 0.1), (2, 42, 0.9), (100, 7, 0.2), (1000, 42, 0.05),
+                                         (5000, 7, 0.02), (777, 42, 0.08)])
+def test_collide_small(orc, strategy, rho, n, seed, rmax):
+    s = inputs.spheres(n, seed, rmax)
+    m = tri.tri_map_init(n, rho)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
+    sync()
+    assert cnt.item() == orc.collide(s)
+
+
+def test_collide_quantized_and_ranks(orc):
+    s = inputs.spheres_quantized(20000, 42, 11, 0.01)
+    d = torch.from_numpy(s).cuda()
+    ref = orc.collide(s)
+    tot = 0
+    for g in range(3):
+        m = tri.tri_map_init(20000, 128, 1, g, 3, 0)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tri.tri_collide(m, "lambda", d, cnt)
+        sync()
+        tot += cnt.item()
+    assert tot == ref
+
+
+def test_collide_full_size_rank_slice(orc):
+    """BASELINE configs[2] (n = 200000): one 64-way snapped rank slice vs the oracle rows."""
+    n = 200000
+    s = inputs.spheres(n, 42)
+    d = torch.from_numpy(s).cuda()
+    for g in (0, 40):
+        m = tri.tri_map_init(n, 256, 1, g, 256, 1)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tri.tri_collide(m, "persist", d, cnt)
+        sync()
+        assert cnt.item() == orc.collide(s, m.row_begin, m.row_end)
+
+
+# ============================================================== CA
+def ca_gpu(n, state, steps, strategy, rho, world=1):
+    maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+    full = torch.from_numpy(state).cuda()
+    cur = [full[mp.out_offset: mp.out_offset + mp.out_cells].clone() for mp in maps]
+    nxt = [torch.empty_like(c) for c in cur]
+    def row_of(r):   # halo row r as a copy from the rank that owns it (None if outside)
+        for h, p in enumerate(maps):
+            if p.row_begin <= r < p.row_end:
+                o = T(r) - p.out_offset
+                return cur[h][o: o + r + 1].clone()
+        return None
+
+    for _ in range(steps):
+        for g, mp in enumerate(maps):
+            above = row_of(mp.row_begin - 1) if mp.row_begin > 0 else None
+            below = row_of(mp.row_end) if mp.row_end < n else None
+            if mp.out_cells:
+                tri.tri_ca_step(mp, strategy, cur[g], nxt[g], above, below)
+        sync()
+        cur, nxt = nxt, cur
+    return np.concatenate([c.cpu().numpy() for c in cur])
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("rho", [128, 256, 512])
+@pytest.mark.parametrize("n,seed,steps", [(1, 7, 2), (2, 42, 3), (3, 7, 2), (17, 42, 5), (130, 7, 6),
+                                          (1000, 42, 4), (2049, 7, 3)])
+def test_ca_small(orc, strategy, rho, n, seed, steps):
+    st = inputs.ca_state(n, seed)
+    assert np.array_equal(ca_gpu(n, st, steps, strategy, rho), orc.ca_run(n, st, steps))
+
+
+@pytest.mark.parametrize("world", [2, 3, 7])
+def test_ca_ranks_with_halos(orc, world):
+    n = 1500
+    st = inputs.ca_state(n, 42)
+    assert np.array_equal(ca_gpu(n, st, 5, "lambda", 128, world), orc.ca_run(n, st, 5))
+
+
+def test_ca_100_steps(orc):
+    n = 2048
+    st = inputs.ca_state(n, 7)
+    assert np.array_equal(ca_gpu(n, st, 100, "persist", 512), orc.ca_run(n, st, 100))
+
+
+def test_ca_full_size_sampled_rows(orc):
+    """BASELINE configs[3]: n = 32768; 2 generations, sampled row bands vs the oracle."""
+    n = 32768
+    st = inputs.ca_state(n, 42)
+    m = tri.tri_map_init(n, 512)
+    a = torch.from_numpy(st).cuda()
+    b = torch.empty_like(a)
+    prev = st
+    for _ in range(2):
+        tri.tri_ca_step(m, "persist", a, b)
+        sync()
+        got = b.cpu().numpy()
+        for rb, re in [(0, 40), (10000, 10010), (32700, 32768)]:
+            assert np.array_equal(got[T(rb):T(re)], orc.ca_step_rows(n, prev, rb, re))
+        prev = got
+        a, b = b, a
+
+
+# ============================================================== triplet
+def triplet_close(got, ref, scale):
+    err = np.abs(got - ref)
+    assert np.all(err <= 1e-5 * scale + 1e-300), (float((err / scale).max()))
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("rho", [8, 16])
+@pytest.mark.parametrize("n,seed,gen", [(3, 7, "lattice"), (4, 42, "lattice"), (17, 7, "points"),
+                                        (40, 42, "lattice"), (100, 7, "points"), (300, 42, "lattice")])
+def test_triplet_small(orc, strategy, rho, n, seed, gen):
+    x = inputs.lattice4(n, seed) if gen == "lattice" else inputs.points4(n, seed)
+    tm = tri.tet_map_init(n, rho)
+    e = torch.empty(n, dtype=torch.float64, device="cuda")
+    tri.tet_triplet(tm, strategy, torch.from_numpy(x).cuda(), e, nu=1.0)
+    sync()
+    got = e.cpu().numpy()
+    ref, A = orc.triplet(x), orc.triplet_abs(x)
+    triplet_close(got, ref, A)
+    assert abs(got.sum() - ref.sum()) <= 1e-5 * A.sum()
+
+
+def test_triplet_ranks_and_nu(orc):
+    n = 200
+    x = inputs.points4(n, 7)
+    d = torch.from_numpy(x).cuda()
+    tot = np.zeros(n)
+    for g in range(4):
+        tm = tri.tet_map_init(n, 8, g, 4)
+        e = torch.empty(n, dtype=torch.float64, device="cuda")
+        tri.tet_triplet(tm, "persist", d, e, nu=2.5)
+        sync()
+        tot += e.cpu().numpy()
+    triplet_close(tot, orc.triplet(x, nu=2.5), orc.triplet_abs(x, nu=2.5))
+
+
+def test_triplet_full_size_sampled(orc):
+    """BASELINE configs[4]: n = 4096, fp32 points; sampled particles vs the oracle."""
+    n = 4096
+    x = inputs.points4(n, 42)
+    tm = tri.tet_map_init(n, 16)
+    e = torch.empty(n, dtype=torch.float64, device="cuda")
+    tri.tet_triplet(tm, "persist", torch.from_numpy(x).cuda(), e)
+    sync()
+    got = e.cpu().numpy()
+    for t0 in (0, 2047, 4090):
+        t1 = t0 + 4 if t0 < 4090 else 4096
+        triplet_close(got[t0:t1], orc.triplet(x, 1.0, t0, t1), orc.triplet_abs(x, 1.0, t0, t1))
+
+
+# ============================================================== ABI errors on device
+def test_abi_rejects_bad_buffers():
+    m = tri.tri_map_init(100, 128)
+    small = torch.empty(10, dtype=torch.float32, device="cuda")
+    pts = torch.rand(100, 3, device="cuda")
+    with pytest.raises(tri.TriError) as e:
+        tri.tri_edm(m, "lambda", pts, small)
+    assert e.value.code == tri.TRI_EINVAL
+    with pytest.raises(tri.TriError):
+        tri.tri_edm(tri.tri_map_init(100, 16), "lambda", pts, torch.empty(T(100), device="cuda"))
+    with pytest.raises(tri.TriError):
+        tri.tri_dummy(tri.tri_map_init(100, 64), "lambda", tri.TRI_DUMMY_DIGEST,
+                      torch.zeros(1, dtype=torch.int64, device="cuda"))

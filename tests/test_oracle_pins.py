@@ -386,3 +386,12 @@ def test_triplet_permutation_and_sum(orc):
     np.testing.assert_allclose(e2, e[perm], rtol=1e-9)
     np.testing.assert_allclose(e.sum(), orc.triplet_total(x), rtol=1e-9)
     np.testing.assert_allclose(orc.triplet(x, t_begin=10, t_end=20), e[10:20], rtol=0)
+
+
+def test_triplet_abs_scale(orc):
+    # A_t = (1/3) sum |E| >= |e_t|, with equality when all E share a sign (lattice, far apart)
+    x = inputs.points4(30, 42)
+    e, a = orc.triplet(x), orc.triplet_abs(x)
+    assert np.all(a >= np.abs(e) - 1e-12 * a)
+    col = np.array([[0, 0, 0, 0], [0.5, 0, 0, 0], [1.0, 0, 0, 0]], np.float32)
+    np.testing.assert_allclose(orc.triplet_abs(col), -orc.triplet(col), rtol=1e-12)
