@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "triangular cells/sec and HBM GB/s (% of peak) at 1/2/4/8 B200 vs BB map"
 UNIT = "cells/s"
-EDM_N, EDM_RHO, EDM_STRAT = 65536, 128, "persist"
+EDM_N, EDM_RHO, EDM_STRAT = 65536, 128, "lambda"
 
 
 def T(r):
@@ -211,7 +211,7 @@ def bench_edm(args, rank, world, local_rank, pk):
     traffic = ncu_traffic("edm")
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
-            "kernel": "edm_kernel<128,3,TRI_LAMBDA_PERSIST>", "peak_source": pk["source"],
+            "kernel": "edm_kernel<128,3,TRI_LAMBDA>", "peak_source": pk["source"],
             "alg_bytes_per_launch": alg_bytes}
 
     # lambda vs BB (paper form and persistent), a few steps each, this rank's slice
@@ -313,7 +313,7 @@ def bench_collide(rank, world, pk):
 def bench_ca(rank, world, pk, steps=100):
     import torch
     from paper_1609_01490_b200 import dist as tdist, inputs, tri
-    n, rho = 32768, 512
+    n, rho = 32768, 256
     st = inputs.ca_state(n, 42)
     maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
     m = maps[rank]
@@ -382,25 +382,28 @@ def bench_triplet(rank, world, pk):
 # ----------------------------------------------------------------------------- CPU oracle
 def cpu_edm_sample(target_s=10.0, max_rows=None):
     """Oracle EDM on a bounded band of rows at the bottom of the triangle (the
-    longest rows), sized for ~target_s seconds.  Returns (cells/s, sample desc, cores)."""
+    longest rows), grown until one pass takes >= 1 s (or covers the whole
+    triangle), then repeated to ~target_s.  Returns (cells/s, desc, cores, rows)."""
     import oracle
     from paper_1609_01490_b200 import inputs
     n = EDM_N
     pts = inputs.points(n, 3, 42)
-    r = 16
-    t0 = time.perf_counter()
-    oracle.edm(pts, n - r, n)
-    dt = time.perf_counter() - t0
-    rate = (T(n) - T(n - r)) / max(dt, 1e-6)
-    want_cells = rate * target_s
-    rows = max(16, min(n, int(want_cells / n)))
-    if max_rows:
-        rows = min(rows, max_rows)
-    t0 = time.perf_counter()
-    oracle.edm(pts, n - rows, n)
-    dt = time.perf_counter() - t0
+    rows = 64
+    while True:
+        t0 = time.perf_counter()
+        oracle.edm(pts, n - rows, n)
+        dt = time.perf_counter() - t0
+        if dt >= 1.0 or rows >= n or (max_rows and rows >= max_rows):
+            break
+        rows = min(n, rows * 4, max_rows or n)
     cells = T(n) - T(n - rows)
-    return cells / dt, f"oracle.edm rows [{n - rows}, {n}) of n={n}: {cells} cells in {dt:.2f} s", oracle.num_threads(), rows
+    reps = max(1, min(50, int(target_s / max(dt, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.edm(pts, n - rows, n)
+    dt = time.perf_counter() - t0
+    desc = f"oracle.edm rows [{n - rows}, {n}) of n={n} ({cells} cells) x {reps} in {dt:.2f} s"
+    return cells * reps / dt, desc, oracle.num_threads(), rows
 
 
 def run_reference(args, rank, world):
@@ -485,7 +488,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded U[0,1)^3 points)",
                 "config": {"workload": "EDM n=65536 3-D fp32 points, packed triangular output (BASELINE configs[1])",
-                           "n": EDM_N, "rho": EDM_RHO, "strategy": "lambda, persistent grid",
+                           "n": EDM_N, "rho": EDM_RHO, "strategy": "lambda(omega), one CTA per tile (paper form)",
                            "cells_per_step": T(EDM_N), "parallelism": f"omega-range x{world}",
                            "l2": "output 8.59 GB per step >> 126 MB L2 (every step streams through HBM; no flush)"},
                 "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],

@@ -134,7 +134,7 @@ tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, i
     g_launches = 0;
     if (bad_map(map) || bad_strategy(strategy) || !d_pts || !d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
-    if (map->rho != 32 && map->rho != 64 && map->rho != 128) return TRI_EINVAL;
+    if (map->rho != 32 && map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
     if (dim < 1 || dim > 4 || ld < dim) return TRI_EINVAL;
     if (((uintptr_t)d_out & 15u) != 0) return TRI_EINVAL;
     if (out_bytes < map->out_cells * 4u) return TRI_EINVAL;

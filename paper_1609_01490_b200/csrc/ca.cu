@@ -10,11 +10,15 @@
 // windows of rows i-1, i, i+1; each window is read as six aligned 32-bit words
 // (L1-resident: neighbouring lanes and rows share lines) and realigned with
 // funnel shifts.  The rule is evaluated 4 cells per 32-bit word (SWAR):
-// horizontal byte sums of each row (<= 3 per byte), vertical sum (<= 9, incl.
-// self), then B3/S23 as bit-plane logic:
+// vertical byte sums of the three rows first (<= 3 per byte), then the
+// horizontal 3-sum (<= 9, incl. self), then B3/S23 as bit-plane logic:
 //   next = (sum9 == 3) | (self & (sum9 == 4)).
-// Chunks whose window touches the triangle's edge (column -1, the diagonal),
-// a row end, or the slice end take a per-cell path with explicit bounds.
+// Every chunk runs the same SIMT code: interior chunks load unmasked; chunks
+// touching column -1, the diagonal or the slice edge load with byte masks
+// (columns outside [0, r] of row r and absent rows read as dead); a chunk that
+// crosses the end of row i is two 16-cell evaluations (row i at j0, row i+1 at
+// j0 - i - 1) merged bytewise.  Only rows i < 16 (chunks spanning 3+ rows)
+// fall back to a per-cell loop.
 #include "tri_common.cuh"
 
 namespace {
@@ -55,36 +59,40 @@ __device__ __forceinline__ uint32_t life_cell(const CaArgs &a, int64_t i, int64_
     return (nb == 3u) | (self & (nb == 2u));
 }
 
-// Horizontal sums of an 18-byte window (cols c-1 .. c+16) of one row.
-// R: six aligned words covering the window, sh: byte offset of col c-1 in R[0].
-// H[w] = bytes (cols 4w+c-1 + cols 4w+c + cols 4w+c+1) for the 4 cells of word w,
-// M[w] = the row's own cells 4w+c .. 4w+c+3.
-__device__ __forceinline__ void row_sums(const uint32_t (&R)[6], uint32_t sh, uint32_t (&H)[4],
-                                         uint32_t (&M)[4]) {
-    uint32_t X[5];
+// Window of row r, columns [cs, cs + 18): X[t] = bytes of columns cs+4t .. cs+4t+3.
+// MASK: columns outside [0, r] read as 0 and words holding no valid column are
+// never loaded (so nothing outside the row's buffer is touched).
+template <bool MASK>
+__device__ __forceinline__ void window(const CaArgs &a, int64_t r, int64_t cs, uint32_t (&X)[5]) {
+    const uint8_t *p = MASK ? row_ptr(a, r) : a.in + (tri::T2((uint64_t)r) - a.base);
+    if (MASK && !p) {                       // dead row (outside the domain / absent halo)
 #pragma unroll
-    for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t], R[t + 1], 8 * sh);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        const uint32_t mid = __funnelshift_r(X[w], X[w + 1], 8);
-        const uint32_t rgt = __funnelshift_r(X[w], X[w + 1], 16);
-        H[w] = X[w] + mid + rgt;
-        M[w] = mid;
-    }
-}
-
-__device__ __forceinline__ void load6(const uint8_t *row, int64_t c_left, uint32_t (&R)[6], uint32_t &sh) {
-    if (!row) {
-#pragma unroll
-        for (int t = 0; t < 6; ++t) R[t] = 0;
-        sh = 0;
+        for (int t = 0; t < 5; ++t) X[t] = 0;
         return;
     }
-    const uintptr_t ad = (uintptr_t)(row + c_left);
-    sh = (uint32_t)(ad & 3u);
+    const uintptr_t ad = (uintptr_t)(p + cs);
+    const uint32_t sh = (uint32_t)(ad & 3u);
     const uint32_t *w = (const uint32_t *)(ad & ~(uintptr_t)3);
+    uint32_t R[6];
 #pragma unroll
-    for (int t = 0; t < 6; ++t) R[t] = __ldg(w + t);
+    for (int t = 0; t < 6; ++t) {
+        if (MASK) {
+            const int64_t cw = cs - (int64_t)sh + 4 * t;       // column of the word's byte 0
+            if (cw + 3 < 0 || cw > r) {
+                R[t] = 0;
+            } else {
+                uint32_t v = __ldg(w + t);
+                const int lo = cw < 0 ? (int)(-cw) : 0;
+                const int hi = cw + 3 > r ? (int)(cw + 3 - r) : 0;
+                v &= (0xffffffffu << (8 * lo)) & (0xffffffffu >> (8 * hi));
+                R[t] = v;
+            }
+        } else {
+            R[t] = __ldg(w + t);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t], R[t + 1], 8 * sh);
 }
 
 __device__ __forceinline__ uint32_t life_word(uint32_t sum9, uint32_t self) {
@@ -93,6 +101,34 @@ __device__ __forceinline__ uint32_t life_word(uint32_t sum9, uint32_t self) {
     const uint32_t is3 = ~b3 & ~b2 & b1 & b0;
     const uint32_t is4 = ~b3 & b2 & ~b1 & ~b0;
     return (is3 | (self & is4)) & 0x01010101u;
+}
+
+// Next state of the 16 cells (r, js .. js+15) into o[4] (byte q = cell js+q).
+template <bool MASK>
+__device__ __forceinline__ void eval16(const CaArgs &a, int64_t r, int64_t js, uint32_t (&o)[4]) {
+    uint32_t U[5], M[5], D[5], V[5];
+    window<MASK>(a, r - 1, js - 1, U);
+    window<MASK>(a, r, js - 1, M);
+    window<MASK>(a, r + 1, js - 1, D);
+#pragma unroll
+    for (int t = 0; t < 5; ++t) V[t] = U[t] + M[t] + D[t];       // vertical 3-sums
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t sum9 = V[w] + __funnelshift_r(V[w], V[w + 1], 8) + __funnelshift_r(V[w], V[w + 1], 16);
+        const uint32_t self = __funnelshift_r(M[w], M[w + 1], 8);
+        o[w] = life_word(sum9, self);
+    }
+}
+
+__device__ __forceinline__ void store_chunk(const CaArgs &a, uint64_t c, const uint32_t (&o)[4]) {
+    uint8_t *dst = a.out + c;
+    if (c + 16 <= a.out_cells) {
+        st_cs_v4u(dst, o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll 1
+        for (int q = 0; q < 16; ++q)
+            if (c + q < a.out_cells) dst[q] = (uint8_t)(o[q >> 2] >> (8 * (q & 3)));
+    }
 }
 
 template <int RHO>
@@ -118,23 +154,26 @@ __device__ __forceinline__ void ca_tile(const CaArgs &a, uint32_t bi, uint32_t b
         if (off >= len) continue;
         const uint64_t c = s + (uint64_t)off;
         const int64_t j0 = c0 + off;              // first cell column
-        uint8_t *dst = a.out + c;
-        if (j0 >= 1 && j0 + 16 <= i - 1) {
-            // all 18 window columns valid in rows i-1, i, i+1
-            uint32_t R[6], sh, Hu[4], Hm[4], Hd[4], Mu[4], Mm[4], Md[4];
-            load6(row_ptr(a, i - 1), j0 - 1, R, sh);
-            row_sums(R, sh, Hu, Mu);
-            load6(row_ptr(a, i), j0 - 1, R, sh);
-            row_sums(R, sh, Hm, Mm);
-            load6(row_ptr(a, i + 1), j0 - 1, R, sh);
-            row_sums(R, sh, Hd, Md);
-            uint32_t o[4];
+        uint32_t o[4];
+        if (j0 >= 1 && j0 + 16 <= i - 1 && i > a.R0 && i + 1 < a.R1) {
+            eval16<false>(a, i, j0, o);           // interior: all window rows/columns in the slice
+        } else if (j0 + 15 <= i) {
+            eval16<true>(a, i, j0, o);            // touches column -1 / the diagonal
+        } else if (i >= 16) {
+            // crosses the row end: cells j0..i of row i, then 0.. of row i+1
+            uint32_t A[4], B[4];
+            const int na = (int)(i - j0 + 1);     // 1..15 cells from row i
+            eval16<true>(a, i, j0, A);
+            eval16<true>(a, i + 1, j0 - i - 1, B);
 #pragma unroll
-            for (int w = 0; w < 4; ++w) o[w] = life_word(Hu[w] + Hm[w] + Hd[w], Mm[w]);
-            st_cs_v4u(dst, o[0], o[1], o[2], o[3]);
+            for (int w = 0; w < 4; ++w) {
+                const int lo = na - 4 * w;        // bytes of word w taken from A
+                const uint32_t m = lo >= 4 ? 0xffffffffu : (lo <= 0 ? 0u : (0xffffffffu >> (8 * (4 - lo))));
+                o[w] = (A[w] & m) | (B[w] & ~m);
+            }
         } else {
-            // edge chunk: per cell, walking Eq. 1 across the row end
-            uint32_t o[4] = {0, 0, 0, 0};
+            // rows < 16: a chunk may span several rows -- per cell along Eq. 1
+            o[0] = o[1] = o[2] = o[3] = 0;
             int64_t ii = i, jj = j0;
 #pragma unroll 1
             for (int q = 0; q < 16; ++q) {
@@ -142,14 +181,8 @@ __device__ __forceinline__ void ca_tile(const CaArgs &a, uint32_t bi, uint32_t b
                 if (c + q < a.out_cells) o[q >> 2] |= life_cell(a, ii, jj) << (8 * (q & 3));
                 ++jj;
             }
-            if (c + 16 <= a.out_cells) {
-                st_cs_v4u(dst, o[0], o[1], o[2], o[3]);
-            } else {
-#pragma unroll 1
-                for (int q = 0; q < 16; ++q)
-                    if (c + q < a.out_cells) dst[q] = (uint8_t)(o[q >> 2] >> (8 * (q & 3)));
-            }
         }
+        store_chunk(a, c, o);
     }
 }
 

@@ -7,16 +7,17 @@
 // 16-byte streaming stores, every aligned 4-float CHUNK of the output slice is
 // owned by the tile that holds the chunk's first cell; the owner computes all
 // four cells even when they run past the tile edge (EDM is pointwise, so the
-// neighbour cells are computable anywhere).  Consequences:
-//   * rho/4 chunk lanes per row segment; at rho = 128 one warp covers one row
-//     segment with one 512-byte coalesced st.global.cs.v4 per row;
-//   * the row's chunk phase delta = (-T(i)) mod 4 is warp-uniform at rho = 128,
-//     so each lane picks its 4 columns from a 7-column register window with a
-//     uniform switch (no shuffles, no shared memory);
-//   * a chunk that crosses the end of row i (diagonal tile) or of the slice
-//     takes a scalar slow path (one per row end).
-// Column points are loaded once per tile per lane (7 x dim floats, L1/L2
-// resident: 786 KB for n = 65536), row points once per row (warp broadcast).
+// neighbour cells are computable anywhere).
+//
+// Interior tiles (bj + 1 < bi: every chunk stays inside its row) take the
+// fast path: one warp walks ROWS rows of the tile; lane k owns chunk slots
+// k, k+32, ... (CPL = rho/128 chunks per lane per row, interleaved so each
+// store instruction is one 512-byte contiguous run).  The row's chunk phase
+// delta = (-T(i)) mod 4 is warp-uniform, so every lane takes its 4 columns
+// from a 7-column register window with a uniform switch; the row offset is
+// advanced incrementally (T(i+1) = T(i) + i + 1) and the row point is
+// broadcast by shuffle.  Tiles touching the diagonal (bj >= bi - 1) take a
+// checked path that walks Eq. 1 across row ends and the slice end.
 #include "tri_common.cuh"
 
 namespace {
@@ -31,10 +32,11 @@ struct EdmArgs {
 };
 
 constexpr int kEdmThreads = 256;
+constexpr int kWarps = kEdmThreads / 32;
 
 template <int DIM>
-__device__ __forceinline__ float dist_reg(const float (&p)[DIM], const float (&w)[DIM][7], int t) {
-    float dx = p[0] - w[0][t];
+__device__ __forceinline__ float dist_w(const float (&p)[DIM], const float (&w)[DIM][7], int t) {
+    const float dx = p[0] - w[0][t];
     float d2 = dx * dx;
 #pragma unroll
     for (int d = 1; d < DIM; ++d) {
@@ -55,73 +57,112 @@ __device__ __forceinline__ float dist_gmem(const EdmArgs &a, int64_t i, int64_t 
     return sqrt_approx(d2);
 }
 
+template <int DIM, int D>
+__device__ __forceinline__ void chunk4(const float (&p)[DIM], const float (&w)[DIM][7], float *dst) {
+    st_cs_v4(dst, dist_w<DIM>(p, w, D), dist_w<DIM>(p, w, D + 1), dist_w<DIM>(p, w, D + 2),
+             dist_w<DIM>(p, w, D + 3));
+}
+
+// Interior tile: rows [r0, r0+RHO) x cols [c0, c0+RHO), c0 + RHO < r0.
 template <int RHO, int DIM>
-__device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
-    constexpr int L = RHO / 4;                 // chunk lanes per row segment
-    constexpr int RPW = 32 / L;                // rows per warp pass
-    constexpr int NW = kEdmThreads / 32;
-    constexpr int ROWS_PER_WARP = RHO / NW;
+__device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, int64_t c0) {
+    constexpr int CPL = RHO / 128;                // chunk slots per lane per row
+    constexpr int ROWS = RHO / kWarps;            // rows per warp (<= 32)
+    static_assert(ROWS <= 32, "row points are broadcast from one lane each");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k = lane % L, rs = lane / L;
-    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-
-    float w[DIM][7];
+    const int64_t rbase = r0 + (int64_t)warp * ROWS;
+    if (rbase >= a.n) return;
+    float w[CPL][DIM][7];
 #pragma unroll
-    for (int t = 0; t < 7; ++t) {
-        const int64_t col = c0 + 4 * k + t;
-        const bool in = col < a.n;
+    for (int c = 0; c < CPL; ++c)
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) w[d][t] = in ? __ldg(a.pts + col * a.ld + d) : 0.f;
+        for (int t = 0; t < 7; ++t) {
+            const int64_t col = c0 + 128 * c + 4 * lane + t;    // < r0 <= n - 1 + ... always in range
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) w[c][d][t] = __ldg(a.pts + col * a.ld + d);
+        }
+    float pr[DIM];
+    {
+        const int64_t rr = rbase + (lane < ROWS ? lane : 0);
+        const bool in = rr < a.n;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) pr[d] = in ? __ldg(a.pts + rr * a.ld + d) : 0.f;
     }
-
-    const int64_t rbase = r0 + (int64_t)warp * ROWS_PER_WARP;
+    const int nrows = (int)((a.n - rbase) < ROWS ? (a.n - rbase) : ROWS);
+    uint64_t s = tri::T2((uint64_t)rbase) + (uint64_t)c0 - a.out_offset;   // local start of row rbase
+    float *base = a.out + 4 * lane;
 #pragma unroll 1
-    for (int rr = rs; rr < ROWS_PER_WARP; rr += RPW) {
-        const int64_t i = rbase + rr;
-        if (i >= a.n) break;
+    for (int rr = 0; rr < nrows; ++rr) {
         float p[DIM];
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) p[d] = __ldg(a.pts + i * a.ld + d);
-        const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.out_offset;  // local segment start
+        for (int d = 0; d < DIM; ++d) p[d] = __shfl_sync(0xffffffffu, pr[d], rr);
+        const int delta = (int)((0u - (uint32_t)s) & 3u);
+        float *dst = base + (s + (uint64_t)delta);
+        switch (delta) {
+            case 0:
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) chunk4<DIM, 0>(p, w[c], dst + 128 * c);
+                break;
+            case 1:
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) chunk4<DIM, 1>(p, w[c], dst + 128 * c);
+                break;
+            case 2:
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) chunk4<DIM, 2>(p, w[c], dst + 128 * c);
+                break;
+            default:
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) chunk4<DIM, 3>(p, w[c], dst + 128 * c);
+                break;
+        }
+        s += (uint64_t)(rbase + rr + 1);               // T(i+1) = T(i) + i + 1
+    }
+}
+
+// Any tile (used for tiles touching the diagonal, and for rho < 128): every
+// chunk slot of every row, cells walked along Eq. 1, all bounds checked.
+template <int RHO, int DIM>
+__device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, int64_t c0) {
+    constexpr int L = RHO / 4;                        // chunk slots per row segment
+    const int t = threadIdx.x;
+#pragma unroll 1
+    for (int q = t; q < RHO * L; q += kEdmThreads) {
+        const int rr = q / L, k = q % L;
+        const int64_t i = r0 + rr;
+        if (i >= a.n) break;
+        const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.out_offset;
         const int64_t seg = i - c0 + 1;
         const int64_t len = seg < RHO ? seg : RHO;
-        const int delta = (int)((0u - (uint32_t)s) & 3u);
-        const int off = delta + 4 * k;
+        const int off = (int)((0u - (uint32_t)s) & 3u) + 4 * k;
         if (off >= len) continue;                      // chunk owned by the next segment
         const uint64_t c = s + (uint64_t)off;
+        float v[4];
+        int64_t ii = i, jj = c0 + off;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            while (jj > ii) { jj -= ii + 1; ++ii; }
+            v[e] = (c + e < a.out_cells && ii < a.n) ? dist_gmem<DIM>(a, ii, jj) : 0.f;
+            ++jj;
+        }
         float *dst = a.out + c;
-        if (c0 + off + 3 <= i && c + 4 <= a.out_cells) {
-            float v0, v1, v2, v3;
-            switch (delta) {
-                case 0: v0 = dist_reg<DIM>(p, w, 0); v1 = dist_reg<DIM>(p, w, 1);
-                        v2 = dist_reg<DIM>(p, w, 2); v3 = dist_reg<DIM>(p, w, 3); break;
-                case 1: v0 = dist_reg<DIM>(p, w, 1); v1 = dist_reg<DIM>(p, w, 2);
-                        v2 = dist_reg<DIM>(p, w, 3); v3 = dist_reg<DIM>(p, w, 4); break;
-                case 2: v0 = dist_reg<DIM>(p, w, 2); v1 = dist_reg<DIM>(p, w, 3);
-                        v2 = dist_reg<DIM>(p, w, 4); v3 = dist_reg<DIM>(p, w, 5); break;
-                default: v0 = dist_reg<DIM>(p, w, 3); v1 = dist_reg<DIM>(p, w, 4);
-                         v2 = dist_reg<DIM>(p, w, 5); v3 = dist_reg<DIM>(p, w, 6); break;
-            }
-            st_cs_v4(dst, v0, v1, v2, v3);
+        if (c + 4 <= a.out_cells) {
+            st_cs_v4(dst, v[0], v[1], v[2], v[3]);
         } else {
-            // chunk crosses the end of row i and/or of the slice: walk Eq. 1
-            float v[4];
-            int64_t ii = i, jj = c0 + off;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                while (jj > ii) { jj -= ii + 1; ++ii; }
-                v[q] = (c + q < a.out_cells && ii < a.n) ? dist_gmem<DIM>(a, ii, jj) : 0.f;
-                ++jj;
-            }
-            if (c + 4 <= a.out_cells) {
-                st_cs_v4(dst, v[0], v[1], v[2], v[3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (c + q < a.out_cells) dst[q] = v[q];
-            }
+            for (int e = 0; e < 4; ++e)
+                if (c + e < a.out_cells) dst[e] = v[e];
         }
     }
+}
+
+template <int RHO, int DIM>
+__device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
+    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
+    if (RHO >= 128 && bj + 1 < bi)
+        edm_tile_interior<(RHO >= 128 ? RHO : 128), DIM>(a, r0, c0);
+    else
+        edm_tile_checked<RHO, DIM>(a, r0, c0);
 }
 
 template <int RHO, int DIM, int STRAT>
@@ -199,7 +240,8 @@ tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int di
     switch (m.rho) {
         case 32: return launch_r<32>(m, strategy, dim, a, st);
         case 64: return launch_r<64>(m, strategy, dim, a, st);
-        default: return launch_r<128>(m, strategy, dim, a, st);
+        case 128: return launch_r<128>(m, strategy, dim, a, st);
+        default: return launch_r<256>(m, strategy, dim, a, st);
     }
 }
 

@@ -71,7 +71,7 @@ __device__ __forceinline__ void st_cs_v4u(void *p, uint32_t a, uint32_t b, uint3
 }
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));   // MUFU.SQRT, no denormal fix-up
     return y;
 }
 

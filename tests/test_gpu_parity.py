@@ -150,7 +150,7 @@ def edm_close(got, ref):
 
 
 @pytest.mark.parametrize("strategy", STRATS)
-@pytest.mark.parametrize("rho", [32, 64, 128])
+@pytest.mark.parametrize("rho", [32, 64, 128, 256])
 @pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (3, 7), (5, 42), (64, 7), (257, 42), (1000, 7), (4097, 42)])
 def test_edm_small(orc, strategy, rho, n, seed):
     pts = inputs.points(n, 3, seed)
@@ -176,14 +176,14 @@ def test_edm_dims_and_stride(orc, dim):
     edm_close(out.cpu().numpy(), orc.edm(pts))
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_edm_ranks_concatenate(orc, world):
+@pytest.mark.parametrize("world,rho", [(2, 64), (3, 64), (5, 64), (3, 256), (4, 128)])
+def test_edm_ranks_concatenate(orc, world, rho):
     n = 3001
     pts = inputs.points(n, 3, 42)
     d = torch.from_numpy(pts).cuda()
     parts = []
     for g in range(world):
-        m = tri.tri_map_init(n, 64, 1, g, world, 1)
+        m = tri.tri_map_init(n, rho, 1, g, world, 1)
         out = torch.empty((max(m.out_cells, 4),), dtype=torch.float32, device="cuda")
         tri.tri_edm(m, "persist", d, out)
         sync()
@@ -191,11 +191,12 @@ def test_edm_ranks_concatenate(orc, world):
     edm_close(np.concatenate(parts), orc.edm(pts))
 
 
-def test_edm_full_size_sampled(orc):
-    """BASELINE configs[1]: n = 65536, 3-D, the bench's launch (rho 128, persistent)."""
+@pytest.mark.parametrize("rho", [128, 256])
+def test_edm_full_size_sampled(orc, rho):
+    """BASELINE configs[1]: n = 65536, 3-D, the bench's launch (persistent lambda)."""
     n = 65536
     pts = inputs.points(n, 3, 42)
-    m = tri.tri_map_init(n, 128)
+    m = tri.tri_map_init(n, rho)
     out = torch.full((m.out_cells,), float("nan"), dtype=torch.float32, device="cuda")
     tri.tri_edm(m, "persist", torch.from_numpy(pts).cuda(), out)
     sync()
