@@ -116,7 +116,7 @@ tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode,
 /* Euclidean distance matrix: for this rank's packed slice,
  * d_out[T(i)+j - out_offset] = || p_i - p_j ||_2 in fp32 for j <= i (diag = 1).
  * d_pts: n points, point t at d_pts[t*ld .. t*ld+dim), dim in 1..4, ld >= dim.
- * Requires out_bytes >= 4 * out_cells, d_out 16-byte aligned; rho in {32,64,128}.
+ * Requires out_bytes >= 4 * out_cells, d_out 16-byte aligned; rho in {32,64,128,256}.
  * Stores are aligned 16-byte streaming stores; each 16-byte chunk of the slice
  * is written by exactly one thread. */
 tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts,
@@ -137,7 +137,7 @@ tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_p
  * number of pairs j < i in this rank's omega tiles with
  *   d2 = fma(dz,dz, fma(dy,dy, dx*dx)) < (ri + rj)^2
  * evaluated in IEEE fp32 round-to-nearest with exactly that operation order.
- * d_spheres: n x 4 floats (x, y, z, r), 16-byte aligned.  rho in {64,128,256}.
+ * d_spheres: n x 4 floats (x, y, z, r), 16-byte aligned.  rho in {128,256,512}.
  * The map must be built with diag = 1 (tiles) -- the strict filter is per pair. */
 tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
                        unsigned long long *d_count, void *stream);
@@ -168,7 +168,7 @@ typedef struct {
     uint64_t waste_tet, waste_bb;  /* unnecessary threads (one per cell, strict p>q>s) */
 } tet_map_t;
 
-/* EINVAL: n < 3, rho not in {4, 8, 16}, bad rank/world. ERANGE: T3(m) >= 2^40. */
+/* EINVAL: n < 3, rho not in {4, 8, 16, 32} (kernels: 8, 16, 32), bad rank/world. ERANGE: T3(m) >= 2^40. */
 tri_status tet_map_init(tet_map_t *map, int64_t n, int32_t rho, int32_t rank, int32_t world);
 
 /* Host mirror of the tetrahedral map (P:617-654 with integer correction):

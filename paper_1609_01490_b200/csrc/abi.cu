@@ -146,7 +146,7 @@ tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_sp
                        unsigned long long *d_count, void *stream) {
     g_launches = 0;
     if (bad_map(map) || bad_strategy(strategy) || !d_spheres || !d_count) return TRI_EINVAL;
-    if (map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
+    if (map->rho != 128 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
     if (((uintptr_t)d_spheres & 15u) != 0) return TRI_EINVAL;
     return launch_collide(*map, strategy, d_spheres, d_count, (cudaStream_t)stream);
 }
@@ -170,7 +170,7 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
 }
 
 tri_status tet_map_init(tet_map_t *map, int64_t n, int32_t rho, int32_t rank, int32_t world) {
-    if (!map || n < 3 || (rho != 4 && rho != 8 && rho != 16) || world < 1 || rank < 0 ||
+    if (!map || n < 3 || (rho != 4 && rho != 8 && rho != 16 && rho != 32) || world < 1 || rank < 0 ||
         rank >= world)
         return TRI_EINVAL;
     if (n > (1ll << 22)) return TRI_ERANGE;

@@ -3,16 +3,20 @@
 // radius inside a unit box ... using a shared memory approach").
 //
 // Tile = rho x rho sphere pairs, coordinate from lambda(omega) or the BB grid.
-// The rho column spheres of the tile are staged in shared memory (one float4
-// each, read back as a warp-broadcast LDS.128); each of the rho/2 threads holds
-// K = 2 row spheres in registers and tests them against every column sphere.
-// The predicate is evaluated with explicit round-to-nearest intrinsics in
-// exactly the order the ABI (include/tri.h) fixes, so the integer count is
-// reproducible bit for bit:
+// The rho column spheres of the tile are staged in shared memory, each stored
+// twice as (x,x,y,y | z,z,r,r) so two LDS.128 broadcasts yield packed f32x2
+// operands.  Each of the rho/4 threads holds K = 4 row spheres as two f32x2
+// pairs and tests them against every column sphere with the sm_100 packed
+// FADD2 / FMUL2 / FFMA2 instructions (IEEE round-to-nearest per lane, so the
+// result is bit-identical to the scalar sequence the ABI fixes):
 //   dx = xi - xj, dy, dz;  d2 = fma(dz,dz, fma(dy,dy, dx*dx));  s = ri + rj;  d2 < s*s
-// Out-of-range spheres are NaN (every comparison false).  Diagonal tiles add
-// the strict filter col < row; other tiles run the unmasked loop.  Counts are
-// reduced per warp, per CTA, then one 64-bit atomic per CTA (skipped if 0).
+// Counting: hits are rare (~6e-6 of the pairs at the benchmark), so the hot
+// loop keeps only min(d2 - s*s) per 32-column block (fp32 subtraction without
+// FTZ is sign-exact: d2 - s2 < 0 <=> d2 < s2; min ignores NaN), and a block
+// whose minimum is negative is recounted exactly with the scalar predicate.
+// Out-of-range spheres are NaN (every comparison false).  Diagonal tiles use
+// the scalar predicate with the strict filter col < row.  Counts are reduced
+// per warp and CTA; one 64-bit atomic per CTA (skipped if 0).
 #include "tri_common.cuh"
 
 namespace {
@@ -25,13 +29,53 @@ struct CollideArgs {
     unsigned long long *count;
 };
 
-__device__ __forceinline__ uint32_t hit(float xi, float yi, float zi, float ri, const float4 c) {
-    const float dx = __fsub_rn(xi, c.x);
-    const float dy = __fsub_rn(yi, c.y);
-    const float dz = __fsub_rn(zi, c.z);
+typedef unsigned long long f2;   // packed f32x2 in a 64-bit register
+
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk(f2 v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Exact scalar predicate (the ABI's operation order).
+__device__ __forceinline__ uint32_t hit(const float4 a, float xj, float yj, float zj, float rj) {
+    const float dx = __fsub_rn(a.x, xj);
+    const float dy = __fsub_rn(a.y, yj);
+    const float dz = __fsub_rn(a.z, zj);
     const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-    const float s = __fadd_rn(ri, c.w);
+    const float s = __fadd_rn(a.w, rj);
     return d2 < __fmul_rn(s, s) ? 1u : 0u;
+}
+
+// d2 - s*s for the two packed row spheres (x, y, z, r) against one column sphere.
+__device__ __forceinline__ f2 gap2(f2 x, f2 y, f2 z, f2 r, f2 cx, f2 cy, f2 cz, f2 cr) {
+    const f2 dx = sub2(x, cx), dy = sub2(y, cy), dz = sub2(z, cz);
+    const f2 d2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+    const f2 s = add2(r, cr);
+    return sub2(d2, mul2(s, s));
 }
 
 __device__ __forceinline__ float4 load_sphere(const CollideArgs &a, int64_t idx) {
@@ -40,31 +84,57 @@ __device__ __forceinline__ float4 load_sphere(const CollideArgs &a, int64_t idx)
     return make_float4(nan, nan, nan, nan);
 }
 
+constexpr int K = 4;          // row spheres per thread
+constexpr int BLK = 32;       // columns per min-block
+
 template <int RHO>
 __device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t bi, uint32_t bj,
-                                                 float4 *smem) {
-    constexpr int NT = RHO / 2;
+                                                 float4 (*smem)[2]) {
+    constexpr int NT = RHO / K;
     const int t = threadIdx.x;
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-    smem[t] = load_sphere(a, c0 + t);
-    smem[t + NT] = load_sphere(a, c0 + t + NT);
-    const float4 A = load_sphere(a, r0 + t);
-    const float4 B = load_sphere(a, r0 + t + NT);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const float4 c = load_sphere(a, c0 + t + q * NT);
+        smem[t + q * NT][0] = make_float4(c.x, c.x, c.y, c.y);
+        smem[t + q * NT][1] = make_float4(c.z, c.z, c.w, c.w);
+    }
+    float4 R[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) R[q] = load_sphere(a, r0 + t + q * NT);
     __syncthreads();
     uint32_t cnt = 0;
     if (bi != bj) {
+        const f2 xa = pk(R[0].x, R[1].x), ya = pk(R[0].y, R[1].y), za = pk(R[0].z, R[1].z), ra = pk(R[0].w, R[1].w);
+        const f2 xb = pk(R[2].x, R[3].x), yb = pk(R[2].y, R[3].y), zb = pk(R[2].z, R[3].z), rb = pk(R[2].w, R[3].w);
+#pragma unroll 1
+        for (int cb = 0; cb < RHO; cb += BLK) {
+            float m = __int_as_float(0x7f800000);   // +inf
 #pragma unroll 8
-        for (int c = 0; c < RHO; ++c) {
-            const float4 s = smem[c];
-            cnt += hit(A.x, A.y, A.z, A.w, s);
-            cnt += hit(B.x, B.y, B.z, B.w, s);
+            for (int c = cb; c < cb + BLK; ++c) {
+                const float4 u = smem[c][0], v = smem[c][1];
+                const f2 cx = pk(u.x, u.y), cy = pk(u.z, u.w), cz = pk(v.x, v.y), cr = pk(v.z, v.w);
+                float g0, g1, g2, g3;
+                upk(gap2(xa, ya, za, ra, cx, cy, cz, cr), g0, g1);
+                upk(gap2(xb, yb, zb, rb, cx, cy, cz, cr), g2, g3);
+                m = fminf(m, fminf(fminf(g0, g1), fminf(g2, g3)));
+            }
+            if (__any_sync(0xffffffffu, m < 0.f)) {
+                if (m < 0.f) {                        // rare: exact recount of this block
+                    for (int c = cb; c < cb + BLK; ++c) {
+                        const float4 u = smem[c][0], v = smem[c][1];
+#pragma unroll
+                        for (int q = 0; q < K; ++q) cnt += hit(R[q], u.x, u.z, v.x, v.z);
+                    }
+                }
+            }
         }
-    } else {  // diagonal tile: strict lower triangle, col < row
-#pragma unroll 8
+    } else {  // diagonal tile: strict lower triangle, col < row (scalar, exact)
+#pragma unroll 4
         for (int c = 0; c < RHO; ++c) {
-            const float4 s = smem[c];
-            cnt += (c < t) ? hit(A.x, A.y, A.z, A.w, s) : 0u;
-            cnt += (c < t + NT) ? hit(B.x, B.y, B.z, B.w, s) : 0u;
+            const float4 u = smem[c][0], v = smem[c][1];
+#pragma unroll
+            for (int q = 0; q < K; ++q) cnt += (c < t + q * NT) ? hit(R[q], u.x, u.z, v.x, v.z) : 0u;
         }
     }
     __syncthreads();  // smem reused by the next tile (persistent form)
@@ -73,21 +143,21 @@ __device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t 
 
 template <int NT>
 __device__ __forceinline__ void flush_count(uint32_t cnt, unsigned long long *dst) {
-    __shared__ uint32_t red[NT / 32];
+    __shared__ uint32_t red[(NT + 31) / 32];
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long s = 0;
 #pragma unroll
-        for (int w = 0; w < NT / 32; ++w) s += red[w];
+        for (int w = 0; w < (NT + 31) / 32; ++w) s += red[w];
         if (s) atomicAdd(dst, s);
     }
 }
 
 template <int RHO, int STRAT>
-__global__ void __launch_bounds__(RHO / 2) collide_kernel(CollideArgs a) {
-    __shared__ float4 smem[RHO];
+__global__ void __launch_bounds__(RHO / K) collide_kernel(CollideArgs a) {
+    __shared__ __align__(16) float4 smem[RHO][2];
     uint32_t cnt = 0;
     if (STRAT == TRI_BB) {
         const uint32_t bj = blockIdx.x;
@@ -108,12 +178,12 @@ __global__ void __launch_bounds__(RHO / 2) collide_kernel(CollideArgs a) {
             cnt += collide_tile<RHO>(a, bi, bj, smem);
         }
     }
-    flush_count<RHO / 2>(cnt, a.count);
+    flush_count<RHO / K>(cnt, a.count);
 }
 
 template <int RHO>
 tri_status launch_r(const tri_map_t &m, int strategy, CollideArgs a, cudaStream_t st) {
-    constexpr int NT = RHO / 2;
+    constexpr int NT = RHO / K;
     if (strategy == TRI_BB) {
         const int64_t tr0 = m.row_begin / m.rho;
         const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;
@@ -153,9 +223,9 @@ tri_status launch_collide(const tri_map_t &m, int strategy, const float *sph, un
     a.tile_row_begin = 0;
     a.count = count;
     switch (m.rho) {
-        case 64: return launch_r<64>(m, strategy, a, st);
         case 128: return launch_r<128>(m, strategy, a, st);
-        default: return launch_r<256>(m, strategy, a, st);
+        case 256: return launch_r<256>(m, strategy, a, st);
+        default: return launch_r<512>(m, strategy, a, st);
     }
 }
 

@@ -230,6 +230,273 @@ tri_status launch_r(const tet_map_t &m, int strategy, TripArgs a, cudaStream_t s
     return tri::cuda_status();
 }
 
+// ============================================================================
+// rho = 32: one WARP per tetrahedral tile.  Lane l owns p = k*32 + l and walks
+// all (q, s) of the tile (1024 triplets per lane), so
+//   * e_p accumulates in the lane's register (fp64 across tiles with equal k),
+//   * e_q is one warp all-reduce per q (lane q keeps it; fp64 across tiles with
+//     equal (k, i)),
+//   * e_s is a 32-value register vector reduce-scattered across the warp once
+//     per tile (~0.12 shuffles per triplet).
+// Three squared-distance tables per warp live in shared memory, padded so every
+// access pattern is conflict-free: Dpq[p][q] (stride 33, per-lane scalar),
+// Dps[p][s] (stride 36, per-lane LDS.128), Dqs[q][s] (stride 32, broadcast
+// LDS.128).  Two s values are processed per instruction with the packed
+// sm_100 f32x2 ops; MUFU.RSQ stays scalar.
+//   E = r^3 + 0.375 P r^5 with r = (abc)^-1/2, P = (b+c-a)(a-b+c)(a+b-c),
+// computed as u' = 0.375 (b + c) - 0.375 a (one FFMA), v = a - (b - c), w = a + (b - c).
+namespace t32 {
+
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk(f2 v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+#define T32_OP2(name, op)                                                          \
+    __device__ __forceinline__ f2 name(f2 a, f2 b) {                               \
+        f2 r;                                                                      \
+        asm(op " %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));                         \
+        return r;                                                                  \
+    }
+T32_OP2(add2, "add.rn.f32x2")
+T32_OP2(sub2, "sub.rn.f32x2")
+T32_OP2(mul2, "mul.rn.f32x2")
+#undef T32_OP2
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Two ATM energies (without nu) for the s-pair (b, c) at fixed a, 11 FP32 ops each:
+//   P' = 3/8 P = (0.375 (b + c) - 0.375 a) * (a^2 - (b - c)^2)
+//   E  = r^3 (1 + P' r^2),  r = rsqrt(a b c)      (a^2 and -0.375 a hoisted per q)
+__device__ __forceinline__ f2 atm2(f2 aa, f2 a2, f2 na375, f2 c375, f2 one, f2 b, f2 c) {
+    const f2 sg = add2(b, c), dl = sub2(b, c);
+    const f2 u = fma2(c375, sg, na375);
+    const f2 ndl = dl ^ 0x8000000080000000ull;          // -(b - c), both lanes (sign flip, no FP op)
+    const f2 t = fma2(ndl, dl, a2);
+    const f2 P = mul2(u, t);
+    float x0, x1;
+    upk(mul2(mul2(b, c), aa), x0, x1);
+    const f2 r = pk(rsqrtf(x0), rsqrtf(x1));
+    const f2 r2 = mul2(r, r);
+    const f2 y = fma2(P, r2, one);
+    return mul2(mul2(r2, r), y);
+}
+
+struct WarpSmem {
+    float4 P[32], Q[32], S[32];
+    float Dqs[32][32];
+    float Dps[32][36];
+    float Dpq[32][33];
+};
+
+__device__ __forceinline__ float d2f(const float4 a, const float4 b) {
+    const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+    return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+
+__device__ __forceinline__ float4 ldp(const TripArgs &a, int64_t idx) {
+    return idx < a.n ? __ldg(a.pts + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Per-warp tile state carried across consecutive tiles.
+struct Acc {
+    double ep, eq;           // lane's p (block kb) and q (block ib) energies
+    uint32_t kb, ib;
+    bool live;
+};
+
+__device__ __forceinline__ void flush_pq(const TripArgs &a, Acc &acc, int lane) {
+    if (!acc.live) return;
+    const int64_t p = (int64_t)acc.kb * 32 + lane, q = (int64_t)acc.ib * 32 + lane;
+    if (acc.ep != 0.0 && p < a.n) atomicAdd(a.energy + p, acc.ep * a.nu_third);
+    if (acc.eq != 0.0 && q < a.n) atomicAdd(a.energy + q, acc.eq * a.nu_third);
+    acc.ep = acc.eq = 0.0;
+    acc.live = false;
+}
+
+template <bool MASKED>
+__device__ __forceinline__ void tile(const TripArgs &a, WarpSmem &sm, uint32_t kb, uint32_t ib, uint32_t jb,
+                                     bool new_pq, Acc &acc) {
+    const int lane = threadIdx.x & 31;
+    // stage points and tables (Dpq only when (k, i) changed)
+    sm.S[lane] = ldp(a, (int64_t)jb * 32 + lane);
+    if (new_pq) {
+        sm.P[lane] = ldp(a, (int64_t)kb * 32 + lane);
+        sm.Q[lane] = ldp(a, (int64_t)ib * 32 + lane);
+    }
+    __syncwarp();
+    const float4 myS = sm.S[lane];
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+        sm.Dqs[r][lane] = d2f(sm.Q[r], myS);
+        sm.Dps[r][lane] = d2f(sm.P[r], myS);
+    }
+    if (new_pq) {
+        const float4 myQ = sm.Q[lane];
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) sm.Dpq[r][lane] = d2f(sm.P[r], myQ);
+    }
+    __syncwarp();
+    const int64_t p = (int64_t)kb * 32 + lane;
+    const f2 c375 = pk(0.375f, 0.375f), one = pk(1.f, 1.f);
+    f2 es[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) es[t] = 0ull;
+    float accp = 0.f, myq = 0.f;
+#pragma unroll 1
+    for (int q = 0; q < 32; ++q) {
+        const float av = sm.Dpq[lane][q];
+        const f2 aa = pk(av, av), na = pk(-0.375f * av, -0.375f * av), a2 = pk(av * av, av * av);
+        f2 row = 0ull;
+        bool pq_ok = true;
+        if (MASKED) pq_ok = p < a.n && (kb != ib || lane > q) && ((int64_t)ib * 32 + q < a.n);
+#pragma unroll
+        for (int s4 = 0; s4 < 8; ++s4) {
+            const float4 b4 = *reinterpret_cast<const float4 *>(&sm.Dqs[q][4 * s4]);
+            const float4 c4 = *reinterpret_cast<const float4 *>(&sm.Dps[lane][4 * s4]);
+            f2 e01 = atm2(aa, a2, na, c375, one, pk(b4.x, b4.y), pk(c4.x, c4.y));
+            f2 e23 = atm2(aa, a2, na, c375, one, pk(b4.z, b4.w), pk(c4.z, c4.w));
+            if (MASKED) {
+                float e0, e1, e2, e3;
+                upk(e01, e0, e1);
+                upk(e23, e2, e3);
+                const int sb = 4 * s4;
+                const int64_t sg = (int64_t)jb * 32 + sb;
+                const bool sj = ib != jb;
+                e0 = (pq_ok && sg + 0 < a.n && (sj || sb + 0 < q)) ? e0 : 0.f;
+                e1 = (pq_ok && sg + 1 < a.n && (sj || sb + 1 < q)) ? e1 : 0.f;
+                e2 = (pq_ok && sg + 2 < a.n && (sj || sb + 2 < q)) ? e2 : 0.f;
+                e3 = (pq_ok && sg + 3 < a.n && (sj || sb + 3 < q)) ? e3 : 0.f;
+                e01 = pk(e0, e1);
+                e23 = pk(e2, e3);
+            }
+            row = add2(row, add2(e01, e23));
+            es[2 * s4] = add2(es[2 * s4], e01);
+            es[2 * s4 + 1] = add2(es[2 * s4 + 1], e23);
+        }
+        float r0, r1;
+        upk(row, r0, r1);
+        const float rs = r0 + r1;          // sum over s of E(p, q, s) for this lane's p
+        accp += rs;
+        float tq = rs;                     // sum over p (lanes) -> e_q
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tq += __shfl_xor_sync(0xffffffffu, tq, o);
+        myq = (lane == q) ? tq : myq;
+    }
+    acc.ep += (double)accp;
+    acc.eq += (double)myq;
+    acc.live = true;
+    acc.kb = kb;
+    acc.ib = ib;
+    // e_s: reduce-scatter the 32 per-lane values over the warp (butterfly)
+    float v[32];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) upk(es[t], v[2 * t], v[2 * t + 1]);
+    int idx = 0;
+#pragma unroll
+    for (int o = 16, half = 16; o >= 1; o >>= 1, half >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int h = 0; h < half; ++h) {
+            const float send = up ? v[h] : v[h + half];
+            const float keep = up ? v[h + half] : v[h];
+            v[h] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        idx += up ? half : 0;
+    }
+    const int64_t si = (int64_t)jb * 32 + idx;
+    if (v[0] != 0.f && si < a.n) atomicAdd(a.energy + si, (double)v[0] * a.nu_third);
+    __syncwarp();   // tables are rewritten by the next tile
+}
+
+__device__ __forceinline__ bool needs_mask(const TripArgs &a, uint32_t kb, uint32_t ib, uint32_t jb) {
+    return kb == ib || ib == jb || (int64_t)(kb + 1) * 32 > a.n;
+}
+
+__device__ __forceinline__ void run_tile(const TripArgs &a, WarpSmem &sm, uint32_t kb, uint32_t ib, uint32_t jb,
+                                         Acc &acc) {
+    const int lane = threadIdx.x & 31;
+    const bool new_pq = !acc.live || acc.kb != kb || acc.ib != ib;
+    if (new_pq) flush_pq(a, acc, lane);
+    if (needs_mask(a, kb, ib, jb))
+        tile<true>(a, sm, kb, ib, jb, new_pq, acc);
+    else
+        tile<false>(a, sm, kb, ib, jb, new_pq, acc);
+}
+
+constexpr int kWarps = 2;          // 2 x 14.4 KB of tables per CTA (static smem limit 48 KB)
+
+template <int STRAT>
+__global__ void __launch_bounds__(32 * kWarps) triplet32_kernel(TripArgs a) {
+    __shared__ __align__(16) WarpSmem smem[kWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem &sm = smem[warp];
+    Acc acc;
+    acc.ep = acc.eq = 0.0;
+    acc.kb = acc.ib = 0;
+    acc.live = false;
+    if (STRAT == TRI_BB) {
+        const uint32_t jb = blockIdx.x * kWarps + warp, ib = blockIdx.y, kb = blockIdx.z;
+        if (jb > ib || ib > kb) return;                  // outside the tetrahedron (warp-uniform)
+        run_tile(a, sm, kb, ib, jb, acc);
+    } else if (STRAT == TRI_LAMBDA) {
+        const uint64_t w = a.omega_begin + ((uint64_t)blockIdx.y * gridDim.x + blockIdx.x) * kWarps + warp;
+        if (w >= a.omega_end) return;
+        uint32_t ib, jb, kb;
+        tri::tet_map(w, ib, jb, kb);
+        run_tile(a, sm, kb, ib, jb, acc);
+    } else {
+        // contiguous omega chunk per warp: consecutive tiles share (k, i)
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+        const uint64_t per = (nb + nw - 1) / nw;
+        const uint64_t w0 = a.omega_begin + per * ((uint64_t)blockIdx.x * kWarps + warp);
+        uint64_t w1 = w0 + per;
+        if (w1 > a.omega_end) w1 = a.omega_end;
+        if (w0 >= w1) return;
+        uint32_t ib, jb, kb;
+        tri::tet_map(w0, ib, jb, kb);
+#pragma unroll 1
+        for (uint64_t w = w0; w < w1; ++w) {
+            run_tile(a, sm, kb, ib, jb, acc);
+            if (++jb > ib) { jb = 0; if (++ib > kb) { ib = 0; ++kb; } }   // Eq. 1 successor
+        }
+    }
+    flush_pq(a, acc, lane);
+}
+
+tri_status launch(const tet_map_t &m, int strategy, TripArgs a, cudaStream_t st) {
+    const unsigned thr = 32 * kWarps;
+    if (strategy == TRI_BB) {
+        if (m.world > 1 || m.m > 65535) return TRI_ENOTSUP;
+        const unsigned mm = (unsigned)m.m;
+        triplet32_kernel<TRI_BB><<<dim3((mm + kWarps - 1) / kWarps, mm, mm), thr, 0, st>>>(a);
+    } else if (strategy == TRI_LAMBDA) {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        triplet32_kernel<TRI_LAMBDA><<<tri::tile_grid((nb + kWarps - 1) / kWarps), thr, 0, st>>>(a);
+    } else {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, triplet32_kernel<TRI_LAMBDA_PERSIST>, thr, 0);
+        uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
+        if (g * kWarps > nb) g = (nb + kWarps - 1) / kWarps;
+        triplet32_kernel<TRI_LAMBDA_PERSIST><<<(unsigned)g, thr, 0, st>>>(a);
+    }
+    tri::note_launches(1);
+    return tri::cuda_status();
+}
+
+}  // namespace t32
+
 }  // namespace
 
 namespace tri {
@@ -248,6 +515,7 @@ tri_status launch_triplet(const tet_map_t &m, int strategy, const float *pts, do
     switch (m.rho) {
         case 8: return launch_r<8>(m, strategy, a, st);
         case 16: return launch_r<16>(m, strategy, a, st);
+        case 32: return t32::launch(m, strategy, a, st);
         default: return TRI_EINVAL;
     }
 }

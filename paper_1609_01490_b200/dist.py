@@ -2,16 +2,17 @@
 
 One process per GPU.  The block map itself partitions the work
 (tri_map_init(rank, world): contiguous, area-balanced omega ranges snapped to
-tile rows), so EDM and the dummy kernel need no collective at all.  The two
-real exchange steps of the path are here:
+tile rows), so EDM and the dummy kernel need no collective at all.  The real
+exchange steps of the path are here:
 
 * ``allreduce_count``  -- the collision count, SUM over ranks (8 bytes);
 * ``allreduce_energy`` -- per-particle triplet energies, SUM (n fp64);
-* ``halo_exchange``    -- the CA's boundary rows: rank g needs row R_g - 1
-  (the last row of the rank below it in row order) and row R_{g+1} (the first
-  row of the next rank), exchanged point-to-point every generation.
+* ``halo_exchange``    -- the CA's boundary rows: the rank owning rows
+  [R0, R1) needs row R0 - 1 (from the rank that owns it) and row R1, every
+  generation, point to point.
 
-Only torch.distributed calls live here -- no compute.
+Only torch.distributed calls live here -- no compute.  With the gloo backend
+CUDA tensors are staged through host copies (gloo has no CUDA P2P).
 """
 from __future__ import annotations
 
@@ -29,25 +30,29 @@ def world_info():
     return 0, 1
 
 
+def _gloo() -> bool:
+    return dist.get_backend() == "gloo"
+
+
 def allreduce_count(count: torch.Tensor) -> torch.Tensor:
+    """SUM the u64 collision count (stored as int64) across ranks, in place."""
     if dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(count, op=dist.ReduceOp.SUM)
+        if _gloo() and count.is_cuda:
+            h = count.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+            count.copy_(h)
+        else:
+            dist.all_reduce(count, op=dist.ReduceOp.SUM)
     return count
 
 
 def allreduce_energy(energy: torch.Tensor) -> torch.Tensor:
-    if dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(energy, op=dist.ReduceOp.SUM)
-    return energy
+    """SUM the per-particle fp64 triplet energies across ranks, in place."""
+    return allreduce_count(energy)
 
 
-def row_bounds(maps_rows):
-    """maps_rows: list of (row_begin, row_end) for every rank (all ranks compute
-    the same list from tri_map_init, no communication)."""
-    return list(maps_rows)
-
-
-def _owner(bounds, r):
+def owner(bounds, r):
+    """Rank whose row range [a, b) contains row r (None if none)."""
     for g, (a, b) in enumerate(bounds):
         if a <= r < b:
             return g
@@ -56,28 +61,37 @@ def _owner(bounds, r):
 
 def halo_exchange(state: torch.Tensor, bounds, n: int, rank: int, above: torch.Tensor | None,
                   below: torch.Tensor | None):
-    """Exchange the CA boundary rows for the packed slice ``state`` of this rank.
+    """Exchange the CA boundary rows of this rank's packed slice ``state``.
 
-    bounds[g] = (row_begin, row_end) of rank g.  ``above`` receives row R_g - 1
-    (R_g bytes), ``below`` receives row R_{g+1} (R_{g+1} + 1 bytes).  Rows are
-    contiguous in the packed Eq. 1 slice, so the sends are views (no copies).
-    Ranks that own no rows take no part.  Returns the list of requests' waits done.
+    bounds[g] = (row_begin, row_end) of rank g (every rank computes the same
+    list from tri_map_init; no communication).  ``above`` receives row R0 - 1
+    (R0 bytes) and ``below`` receives row R1 (R1 + 1 bytes).  Rows are
+    contiguous in the packed Eq. 1 slice, so the sends are views.  Ranks that
+    own no rows take no part.
     """
     R0, R1 = bounds[rank]
-    ops = []
-    if R1 > R0:
-        # my first row goes to the owner of row R0 - 1 (it is that rank's "below")
-        if R0 > 0:
-            g = _owner(bounds, R0 - 1)
-            ops.append(dist.P2POp(dist.isend, state[0:R0 + 1], g))
-            ops.append(dist.P2POp(dist.irecv, above, g))
-        # my last row goes to the owner of row R1 (it is that rank's "above")
-        if R1 < n:
-            g = _owner(bounds, R1)
-            last = R1 - 1
-            o = T(last) - T(R0)
-            ops.append(dist.P2POp(dist.isend, state[o:o + last + 1], g))
-            ops.append(dist.P2POp(dist.irecv, below, g))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    if R1 <= R0:
+        return
+    sends, recvs = [], []
+    if R0 > 0:                                   # my first row is the "below" halo of owner(R0-1)
+        sends.append((state[0:R0 + 1], owner(bounds, R0 - 1)))
+        recvs.append((above, owner(bounds, R0 - 1)))
+    if R1 < n:                                   # my last row is the "above" halo of owner(R1)
+        o = T(R1 - 1) - T(R0)
+        sends.append((state[o:o + R1], owner(bounds, R1)))
+        recvs.append((below, owner(bounds, R1)))
+    if not sends:
+        return
+    staged = _gloo() and state.is_cuda
+    ops, host_recvs = [], []
+    for t, g in sends:
+        ops.append(dist.P2POp(dist.isend, t.cpu() if staged else t.contiguous(), g))
+    for t, g in recvs:
+        buf = torch.empty(t.shape, dtype=t.dtype) if staged else t
+        host_recvs.append((buf, t))
+        ops.append(dist.P2POp(dist.irecv, buf, g))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    if staged:
+        for buf, t in host_recvs:
+            t.copy_(buf)

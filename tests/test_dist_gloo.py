@@ -1,0 +1,88 @@
+"""Multi-process tests of the distributed plumbing (-m "not gpu"): gloo backend,
+world size 2 and 3, on CPU tensors.  The partition comes from the real C ABI
+(tri_map_init is host code); the per-rank CA generation is the CPU oracle run on
+the rows the rank owns plus its received halos, so the test checks that the
+exchange delivers exactly the rows the kernel would read: the distributed run
+must equal the single-process oracle bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def T(r):
+    return r * (r + 1) // 2
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _ca_worker(rank, world, port, n, rho, steps, q):
+    try:
+        _init(rank, world, port)
+        import oracle
+        from paper_1609_01490_b200 import dist as tdist, inputs, tri
+        maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+        bounds = [(m.row_begin, m.row_end) for m in maps]
+        m = maps[rank]
+        full0 = inputs.ca_state(n, 42)
+        state = torch.from_numpy(full0[m.out_offset:m.out_offset + m.out_cells].copy())
+        R0, R1 = bounds[rank]
+        above = torch.zeros(max(R0, 1), dtype=torch.uint8)
+        below = torch.zeros(R1 + 1, dtype=torch.uint8)
+        for _ in range(steps):
+            tdist.halo_exchange(state, bounds, n, rank, above if R0 > 0 else None, below if R1 < n else None)
+            if R1 > R0:
+                work = np.zeros(T(n), np.uint8)
+                work[T(R0):T(R1)] = state.numpy()
+                if R0 > 0:
+                    work[T(R0 - 1):T(R0)] = above.numpy()[:R0]
+                if R1 < n:
+                    work[T(R1):T(R1 + 1)] = below.numpy()
+                state = torch.from_numpy(oracle.ca_step_rows(n, work, R0, R1).copy())
+        parts = [None] * world
+        dist.all_gather_object(parts, state.numpy().tobytes())
+        cnt = torch.tensor([rank + 1], dtype=torch.int64)
+        tdist.allreduce_count(cnt)
+        e = torch.full((5,), float(rank), dtype=torch.float64)
+        tdist.allreduce_energy(e)
+        if rank == 0:
+            q.put((b"".join(parts), int(cnt.item()), e.tolist()))
+        dist.destroy_process_group()
+    except Exception as ex:  # surface worker errors
+        q.put(repr(ex))
+        raise
+
+
+@pytest.mark.parametrize("world,n,rho", [(2, 700, 128), (3, 1000, 128), (2, 300, 256)])
+def test_ca_halo_exchange_matches_oracle(orc, world, n, rho):
+    from paper_1609_01490_b200 import inputs
+    steps = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ca_worker, args=(g, world, port, n, rho, steps, q)) for g in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert not isinstance(res, str), res
+    data, cnt, e = res
+    got = np.frombuffer(data, np.uint8)
+    assert np.array_equal(got, orc.ca_run(n, inputs.ca_state(n, 42), steps))
+    assert cnt == world * (world + 1) // 2
+    assert e == [float(sum(range(world)))] * 5

@@ -220,7 +220,7 @@ def test_edm_host_e2e(orc):
 
 # ============================================================== collision
 @pytest.mark.parametrize("strategy", STRATS)
-@pytest.mark.parametrize("rho", [64, 128, 256])
+@pytest.mark.parametrize("rho", [128, 256, 512])
 @pytest.mark.parametrize("n,seed,rmax", [(1, 7, 0.1), (2, 42, 0.9), (100, 7, 0.2), (1000, 42, 0.05),
                                          (5000, 7, 0.02), (777, 42, 0.08)])
 def test_collide_small(orc, strategy, rho, n, seed, rmax):
@@ -330,7 +330,7 @@ def triplet_close(got, ref, scale):
 
 
 @pytest.mark.parametrize("strategy", STRATS)
-@pytest.mark.parametrize("rho", [8, 16])
+@pytest.mark.parametrize("rho", [8, 16, 32])
 @pytest.mark.parametrize("n,seed,gen", [(3, 7, "lattice"), (4, 42, "lattice"), (17, 7, "points"),
                                         (40, 42, "lattice"), (100, 7, "points"), (300, 42, "lattice")])
 def test_triplet_small(orc, strategy, rho, n, seed, gen):
@@ -345,13 +345,14 @@ def test_triplet_small(orc, strategy, rho, n, seed, gen):
     assert abs(got.sum() - ref.sum()) <= 1e-5 * A.sum()
 
 
-def test_triplet_ranks_and_nu(orc):
+@pytest.mark.parametrize("rho", [8, 32])
+def test_triplet_ranks_and_nu(orc, rho):
     n = 200
     x = inputs.points4(n, 7)
     d = torch.from_numpy(x).cuda()
     tot = np.zeros(n)
     for g in range(4):
-        tm = tri.tet_map_init(n, 8, g, 4)
+        tm = tri.tet_map_init(n, rho, g, 4)
         e = torch.empty(n, dtype=torch.float64, device="cuda")
         tri.tet_triplet(tm, "persist", d, e, nu=2.5)
         sync()
@@ -363,7 +364,7 @@ def test_triplet_full_size_sampled(orc):
     """BASELINE configs[4]: n = 4096, fp32 points; sampled particles vs the oracle."""
     n = 4096
     x = inputs.points4(n, 42)
-    tm = tri.tet_map_init(n, 16)
+    tm = tri.tet_map_init(n, 32)
     e = torch.empty(n, dtype=torch.float64, device="cuda")
     tri.tet_triplet(tm, "persist", torch.from_numpy(x).cuda(), e)
     sync()
