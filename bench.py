@@ -313,7 +313,7 @@ def bench_collide(rank, world, pk):
 def bench_ca(rank, world, pk, steps=100):
     import torch
     from paper_1609_01490_b200 import dist as tdist, inputs, tri
-    n, rho = 32768, 256
+    n, rho = 32768, 128
     st = inputs.ca_state(n, 42)
     maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
     m = maps[rank]

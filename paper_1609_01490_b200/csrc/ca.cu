@@ -95,12 +95,44 @@ __device__ __forceinline__ void window(const CaArgs &a, int64_t r, int64_t cs, u
     for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t], R[t + 1], 8 * sh);
 }
 
+// Interior window: the 18 bytes at w (all inside one row of the slice buffer)
+// from two aligned 16-byte loads (a third 4-byte load when the window starts at
+// byte 15 of its chunk); the realignment offset is uniform across a row group.
+__device__ __forceinline__ void window128(const uint8_t *w, uint32_t (&X)[5]) {
+    const uintptr_t A = (uintptr_t)w;
+    const uint4 *q = (const uint4 *)(A & ~(uintptr_t)15);
+    const uint32_t o = (uint32_t)(A & 15u);
+    const uint4 c0 = __ldg(q), c1 = __ldg(q + 1);
+    const uint32_t R8 = (o == 15u) ? __ldg((const uint32_t *)(q + 2)) : 0u;
+    const uint32_t R[9] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, R8};
+    const uint32_t sh = 8u * (o & 3u);
+    switch (o >> 2) {
+        case 0:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t], R[t + 1], sh);
+            break;
+        case 1:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t + 1], R[t + 2], sh);
+            break;
+        case 2:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t + 2], R[t + 3], sh);
+            break;
+        default:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t + 3], R[t + 4], sh);
+            break;
+    }
+}
+
+// B3/S23 on 4 cells: with nb = sum9 - self (bytes 0..8),
+// alive' = (nb == 3) | (self & nb == 2)  <=>  (nb | self) == 3.
+// y = (nb | self) ^ 3 has bytes <= 15, so y + 0x7f never carries between bytes
+// and its bit 7 is clear exactly when y == 0.
 __device__ __forceinline__ uint32_t life_word(uint32_t sum9, uint32_t self) {
-    // bytes of sum9 are 0..9 (4 bits).  Bit planes at bit 0 of every byte:
-    const uint32_t b0 = sum9, b1 = sum9 >> 1, b2 = sum9 >> 2, b3 = sum9 >> 3;
-    const uint32_t is3 = ~b3 & ~b2 & b1 & b0;
-    const uint32_t is4 = ~b3 & b2 & ~b1 & ~b0;
-    return (is3 | (self & is4)) & 0x01010101u;
+    const uint32_t y = ((sum9 - self) | self) ^ 0x03030303u;
+    return (~(y + 0x7f7f7f7fu) >> 7) & 0x01010101u;
 }
 
 // Next state of the 16 cells (r, js .. js+15) into o[4] (byte q = cell js+q).
@@ -120,6 +152,22 @@ __device__ __forceinline__ void eval16(const CaArgs &a, int64_t r, int64_t js, u
     }
 }
 
+// Interior chunk: rows given by their column-0 pointers (all in the slice).
+__device__ __forceinline__ void eval16_fast(const uint8_t *pu, const uint8_t *pm, const uint8_t *pd, int64_t js,
+                                            uint32_t (&o)[4]) {
+    uint32_t U[5], M[5], D[5], V[5];
+    window128(pu + js - 1, U);
+    window128(pm + js - 1, M);
+    window128(pd + js - 1, D);
+#pragma unroll
+    for (int t = 0; t < 5; ++t) V[t] = U[t] + M[t] + D[t];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t sum9 = V[w] + __funnelshift_r(V[w], V[w + 1], 8) + __funnelshift_r(V[w], V[w + 1], 16);
+        o[w] = life_word(sum9, __funnelshift_r(M[w], M[w + 1], 8));
+    }
+}
+
 __device__ __forceinline__ void store_chunk(const CaArgs &a, uint64_t c, const uint32_t (&o)[4]) {
     uint8_t *dst = a.out + c;
     if (c + 16 <= a.out_cells) {
@@ -129,6 +177,125 @@ __device__ __forceinline__ void store_chunk(const CaArgs &a, uint64_t c, const u
         for (int q = 0; q < 16; ++q)
             if (c + q < a.out_cells) dst[q] = (uint8_t)(o[q >> 2] >> (8 * (q & 3)));
     }
+}
+
+// Raw (unaligned) 18-byte window: loads issued now, realigned later, so that a
+// lane can keep the six windows of two rows in flight at once.
+struct RawWin {
+    uint4 c0, c1;
+    uint32_t r8, o;
+};
+
+__device__ __forceinline__ RawWin load_win(const uint8_t *w) {
+    const uintptr_t A = (uintptr_t)w;
+    const uint4 *q = (const uint4 *)(A & ~(uintptr_t)15);
+    RawWin r;
+    r.o = (uint32_t)(A & 15u);
+    r.c0 = __ldg(q);
+    r.c1 = __ldg(q + 1);
+    r.r8 = (r.o == 15u) ? __ldg((const uint32_t *)(q + 2)) : 0u;
+    return r;
+}
+
+__device__ __forceinline__ void realign(const RawWin &r, uint32_t (&X)[5]) {
+    const uint32_t R[9] = {r.c0.x, r.c0.y, r.c0.z, r.c0.w, r.c1.x, r.c1.y, r.c1.z, r.c1.w, r.r8};
+    const uint32_t sh = 8u * (r.o & 3u);
+    switch (r.o >> 2) {
+        case 0:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t], R[t + 1], sh);
+            break;
+        case 1:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t + 1], R[t + 2], sh);
+            break;
+        case 2:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t + 2], R[t + 3], sh);
+            break;
+        default:
+#pragma unroll
+            for (int t = 0; t < 5; ++t) X[t] = __funnelshift_r(R[t + 3], R[t + 4], sh);
+            break;
+    }
+}
+
+__device__ __forceinline__ void life16(const RawWin &ru, const RawWin &rm, const RawWin &rd, uint32_t (&o)[4]) {
+    uint32_t U[5], M[5], D[5], V[5];
+    realign(ru, U);
+    realign(rm, M);
+    realign(rd, D);
+#pragma unroll
+    for (int t = 0; t < 5; ++t) V[t] = U[t] + M[t] + D[t];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t sum9 = V[w] + __funnelshift_r(V[w], V[w + 1], 8) + __funnelshift_r(V[w], V[w + 1], 16);
+        o[w] = life_word(sum9, __funnelshift_r(M[w], M[w + 1], 8));
+    }
+}
+
+// Where one output chunk of row i lies (aligned-chunk ownership) and whether it
+// can take the interior path.
+struct ChunkPos {
+    uint64_t c;          // local packed index of the chunk (16-aligned)
+    int64_t i, j0;       // first cell
+    const uint8_t *pm;   // column 0 of row i in the slice buffer
+    bool valid, fast;
+};
+
+template <int RHO>
+__device__ __forceinline__ ChunkPos chunk_pos(const CaArgs &a, int64_t i, int64_t c0, int k) {
+    ChunkPos p;
+    p.i = i;
+    p.valid = false;
+    p.fast = false;
+    if (i >= a.R1 || i < a.R0) return p;
+    const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.base;   // local segment start
+    const int64_t seg = i - c0 + 1;
+    const int64_t len = seg < RHO ? seg : RHO;
+    const int off = (int)((0u - (uint32_t)s) & 15u) + 16 * k;
+    if (off >= len) return p;
+    p.valid = true;
+    p.c = s + (uint64_t)off;
+    p.j0 = c0 + off;
+    p.pm = a.in + (s - (uint64_t)c0);
+    p.fast = p.j0 >= 1 && p.j0 + 16 <= i - 1 && i > a.R0 && i + 1 < a.R1;
+    return p;
+}
+
+// Any chunk, including the edge cases (masked windows / row crossing / tiny rows).
+__device__ __forceinline__ void chunk_general(const CaArgs &a, const ChunkPos &p) {
+    const int64_t i = p.i, j0 = p.j0;
+    const uint64_t c = p.c;
+    uint32_t o[4];
+    if (p.fast) {
+        life16(load_win(p.pm - i + j0 - 1), load_win(p.pm + j0 - 1), load_win(p.pm + i + 1 + j0 - 1), o);
+    } else if (j0 + 15 <= i) {
+        eval16<true>(a, i, j0, o);            // touches column -1 / the diagonal / the slice edge
+    } else if (i >= 16) {
+        // crosses the row end: cells j0..i of row i, then 0.. of row i+1
+        uint32_t A[4], B[4];
+        const int na = (int)(i - j0 + 1);     // 1..15 cells from row i
+        eval16<true>(a, i, j0, A);
+        eval16<true>(a, i + 1, j0 - i - 1, B);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int lo = na - 4 * w;        // bytes of word w taken from A
+            const uint32_t m = lo >= 4 ? 0xffffffffu : (lo <= 0 ? 0u : (0xffffffffu >> (8 * (4 - lo))));
+            o[w] = (A[w] & m) | (B[w] & ~m);
+        }
+    } else {
+        // rows < 16: a chunk may span several rows -- per cell along Eq. 1
+        o[0] = o[1] = o[2] = o[3] = 0;
+        int64_t ii = i, jj = j0;
+#pragma unroll 1
+        for (int q = 0; q < 16; ++q) {
+            while (jj > ii) { jj -= ii + 1; ++ii; }
+            if (c + q < a.out_cells) o[q >> 2] |= life_cell(a, ii, jj) << (8 * (q & 3));
+            ++jj;
+        }
+    }
+    store_chunk(a, c, o);
 }
 
 template <int RHO>
@@ -141,50 +308,387 @@ __device__ __forceinline__ void ca_tile(const CaArgs &a, uint32_t bi, uint32_t b
     const int k = lane % L, rs = lane / L;
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
     const int64_t rbase = r0 + (int64_t)warp * ROWS_PER_WARP;
+    // two rows per lane per iteration: all twelve 16-byte loads in flight together
 #pragma unroll 1
-    for (int rr = rs; rr < ROWS_PER_WARP; rr += RPW) {
-        const int64_t i = rbase + rr;
-        if (i >= a.R1) break;
-        if (i < a.R0) continue;
-        const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.base;   // local segment start
-        const int64_t seg = i - c0 + 1;
-        const int64_t len = seg < RHO ? seg : RHO;
-        const int delta = (int)((0u - (uint32_t)s) & 15u);
-        const int off = delta + 16 * k;
-        if (off >= len) continue;
-        const uint64_t c = s + (uint64_t)off;
-        const int64_t j0 = c0 + off;              // first cell column
-        uint32_t o[4];
-        if (j0 >= 1 && j0 + 16 <= i - 1 && i > a.R0 && i + 1 < a.R1) {
-            eval16<false>(a, i, j0, o);           // interior: all window rows/columns in the slice
-        } else if (j0 + 15 <= i) {
-            eval16<true>(a, i, j0, o);            // touches column -1 / the diagonal
-        } else if (i >= 16) {
-            // crosses the row end: cells j0..i of row i, then 0.. of row i+1
-            uint32_t A[4], B[4];
-            const int na = (int)(i - j0 + 1);     // 1..15 cells from row i
-            eval16<true>(a, i, j0, A);
-            eval16<true>(a, i + 1, j0 - i - 1, B);
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const int lo = na - 4 * w;        // bytes of word w taken from A
-                const uint32_t m = lo >= 4 ? 0xffffffffu : (lo <= 0 ? 0u : (0xffffffffu >> (8 * (4 - lo))));
-                o[w] = (A[w] & m) | (B[w] & ~m);
-            }
+    for (int rr = rs; rr < ROWS_PER_WARP; rr += 2 * RPW) {
+        const ChunkPos p = chunk_pos<RHO>(a, rbase + rr, c0, k);
+        const ChunkPos q = (rr + RPW < ROWS_PER_WARP) ? chunk_pos<RHO>(a, rbase + rr + RPW, c0, k) : ChunkPos{};
+        const bool q_ok = rr + RPW < ROWS_PER_WARP && q.valid;
+        if (p.valid && p.fast && q_ok && q.fast) {
+            const RawWin pu = load_win(p.pm - p.i + p.j0 - 1), pm = load_win(p.pm + p.j0 - 1),
+                         pd = load_win(p.pm + p.i + 1 + p.j0 - 1);
+            const RawWin qu = load_win(q.pm - q.i + q.j0 - 1), qm = load_win(q.pm + q.j0 - 1),
+                         qd = load_win(q.pm + q.i + 1 + q.j0 - 1);
+            uint32_t o[4];
+            life16(pu, pm, pd, o);
+            store_chunk(a, p.c, o);
+            life16(qu, qm, qd, o);
+            store_chunk(a, q.c, o);
         } else {
-            // rows < 16: a chunk may span several rows -- per cell along Eq. 1
-            o[0] = o[1] = o[2] = o[3] = 0;
-            int64_t ii = i, jj = j0;
-#pragma unroll 1
-            for (int q = 0; q < 16; ++q) {
-                while (jj > ii) { jj -= ii + 1; ++ii; }
-                if (c + q < a.out_cells) o[q >> 2] |= life_cell(a, ii, jj) << (8 * (q & 3));
-                ++jj;
-            }
+            if (p.valid) chunk_general(a, p);
+            if (q_ok) chunk_general(a, q);
         }
-        store_chunk(a, c, o);
     }
 }
+
+// ============================================================================
+// Bit-sliced tile (rho = 256): the CTA turns its (rho+2)-row halo tile into
+// column-aligned bitmaps in shared memory (bit x of row y <-> column c0-1+x),
+// evaluates B3/S23 32 cells per LOP3 chain, and expands the result to the
+// aligned 16-byte output chunks it owns.  ~3 instructions per cell instead of
+// ~16 for byte SWAR, which made the kernel ALU-bound.
+namespace bits {
+
+template <int RHO>
+struct Cfg {
+    static constexpr int NIN = RHO + 2;                 // input rows r0-1 .. r0+RHO
+    static constexpr int NW = (RHO + 18 + 31) / 32;     // bitmap words per row (cols c0-1 .. c0+RHO+16)
+    static constexpr int NBAND = 32;                    // phase B: NW words x 32 row bands
+    static constexpr int NT = NW * NBAND;               // threads (>= NIN: one input row each in phase A)
+    static_assert(NT >= NIN, "phase A needs one thread per input row");
+    static_assert(RHO % NBAND == 0, "bands of whole rows");
+};
+
+// 16 bytes in {0,1} -> 16 bits (byte q -> bit q): per word (x * 0x01020408) >> 24.
+__device__ __forceinline__ uint32_t pack16(const uint4 c) {
+    const uint32_t n0 = (c.x * 0x01020408u) >> 24, n1 = (c.y * 0x01020408u) >> 24;
+    const uint32_t n2 = (c.z * 0x01020408u) >> 24, n3 = (c.w * 0x01020408u) >> 24;
+    return n0 | (n1 << 4) | (n2 << 8) | (n3 << 12);
+}
+
+// 4 bits -> 4 bytes {0,1}: nibble * 0x00204081 puts bit q at 8q (no collisions).
+__device__ __forceinline__ uint32_t spread4(uint32_t v) { return (v * 0x00204081u) & 0x01010101u; }
+
+// Staged halo rows (rho = 128): each row's 16-byte-aligned byte range is copied
+// into shared memory with coalesced cp.async (LDGSTS, 16 bytes per lane, the
+// whole CTA streaming chunk after chunk), then packed to bits from shared
+// memory.  Row stride 16 (mod 128) bytes keeps the per-thread LDS.128 reads of
+// 8 consecutive rows conflict-free.  (One cp.async.bulk per row was tried: its
+// per-lane uniform-register serialisation cost ~8 issue slots per row.)
+template <int RHO>
+struct Stage {
+    static constexpr bool kOn = RHO == 128;
+    static constexpr int RAWB = 32 * (Cfg<RHO>::NW + 1);     // bytes staged per row (2 chunks per word + 1)
+    static constexpr int NCH = RAWB / 16;
+    static constexpr int STRIDE = RAWB + 16;                   // = 16 (mod 128) for RHO = 128
+};
+
+template <int RHO, bool STAGED = Stage<RHO>::kOn>
+struct Smem {
+    uint32_t in[Cfg<RHO>::NIN][Cfg<RHO>::NW];
+    uint32_t out[RHO][Cfg<RHO>::NW];
+};
+template <int RHO>
+struct Smem<RHO, true> {
+    uint32_t in[Cfg<RHO>::NIN][Cfg<RHO>::NW];
+    uint32_t out[RHO][Cfg<RHO>::NW];
+    alignas(16) uint8_t raw[Cfg<RHO>::NIN][Stage<RHO>::STRIDE];
+    uint64_t seg[RHO];                        // local packed offset of (r0 + rr, c0), phase C
+    alignas(8) unsigned long long bar;        // TMA completion barrier
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// Byte mask of chunk bytes [lo, hi) (clamped to the 16-byte chunk) applied in place.
+__device__ __forceinline__ uint32_t word_mask(int64_t lo_c, int64_t hi_c, int u) {
+    const int lo = (int)(lo_c - 4 * u), hi = (int)(hi_c - 4 * u);
+    const int l = lo < 0 ? 0 : (lo > 4 ? 4 : lo), g = hi < 0 ? 0 : (hi > 4 ? 4 : hi);
+    return g <= l ? 0u : ((0xffffffffu >> (8 * (4 - g))) & (0xffffffffu << (8 * l)));
+}
+__device__ __forceinline__ void mask_chunk(uint4 &c, int64_t lo_c, int64_t hi_c) {
+    c.x &= word_mask(lo_c, hi_c, 0);
+    c.y &= word_mask(lo_c, hi_c, 1);
+    c.z &= word_mask(lo_c, hi_c, 2);
+    c.w &= word_mask(lo_c, hi_c, 3);
+}
+
+// Phase A with TMA staging: thread t = input row t resolves the row (slice /
+// halo / dead; whole window inside the row or not), issues one cp.async.bulk
+// for a whole row or stages a boundary row itself with byte masks, waits on
+// the CTA's mbarrier, then packs its staged bytes to bits.
+template <int RHO>
+__device__ __forceinline__ void phase_a_tma(const CaArgs &a, int64_t r0, int64_t c0, Smem<RHO, true> &sm,
+                                            uint32_t parity) {
+    constexpr int NW = Cfg<RHO>::NW, NIN = Cfg<RHO>::NIN;
+    constexpr int RAWB = Stage<RHO>::RAWB, NCH = Stage<RHO>::NCH;
+    const int t = threadIdx.x;
+    if (t >= NIN) return;
+    const int64_t r = r0 - 1 + t;
+    uint8_t *dst = sm.raw[t];
+    const uint8_t *p = row_ptr(a, r);
+    uint32_t e = 0;
+    if (t >= 1 && t <= RHO) sm.seg[t - 1] = tri::T2((uint64_t)(r0 + t - 1)) + (uint64_t)c0 - a.base;
+    if (!p) {
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) *reinterpret_cast<uint4 *>(dst + 16 * h) = make_uint4(0, 0, 0, 0);
+        mbar_arrive(&sm.bar);
+    } else {
+        const int64_t cs = c0 - 1;
+        const uintptr_t A = (uintptr_t)(p + cs);
+        e = (uint32_t)(A & 15u);
+        const int64_t col0 = cs - (int64_t)e;
+        const uint4 *q = (const uint4 *)(A & ~(uintptr_t)15);
+        if (col0 >= 0 && col0 + RAWB - 1 <= r) {             // whole range inside the row: one TMA copy
+            mbar_arrive_tx(&sm.bar, RAWB);
+            bulk_g2s(dst, q, RAWB, &sm.bar);
+        } else {                                              // boundary row: masked manual staging
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+                const int64_t cb = col0 + 16 * h;
+                const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
+                uint4 c = make_uint4(0, 0, 0, 0);
+                if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
+                    c = __ldg(q + h);
+                    mask_chunk(c, lo_c, hi_c);
+                }
+                *reinterpret_cast<uint4 *>(dst + 16 * h) = c;
+            }
+            mbar_arrive(&sm.bar);
+        }
+    }
+    mbar_wait(&sm.bar, parity);
+    uint32_t prev = 0;
+#pragma unroll
+    for (int v = 0; v <= NW; ++v) {
+        const uint32_t lo = pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v));
+        const uint32_t hi = pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v + 16));
+        const uint32_t P = lo | (hi << 16);
+        if (v > 0) sm.in[t][v - 1] = __funnelshift_r(prev, P, e);
+        prev = P;
+    }
+}
+
+template <int RHO>
+__device__ __forceinline__ void phase_a_row(const CaArgs &a, int64_t r, int64_t c0, uint32_t *dst) {
+    constexpr int NW = Cfg<RHO>::NW;
+    const uint8_t *p = row_ptr(a, r);
+    if (!p) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) dst[w] = 0;
+        return;
+    }
+    const int64_t cs = c0 - 1;                            // column of bitmap bit 0
+    const uintptr_t A = (uintptr_t)(p + cs);
+    const uint4 *q = (const uint4 *)(A & ~(uintptr_t)15);
+    const uint32_t e = (uint32_t)(A & 15u);
+    const int64_t col0 = cs - (int64_t)e;                 // column of chunk 0's byte 0
+    // every loaded byte inside [0, r]: no masks, no out-of-row loads
+    const bool full = col0 >= 0 && col0 + 32 * (NW + 1) - 1 <= r;
+    uint32_t prev = 0;
+#pragma unroll
+    for (int v = 0; v <= NW; ++v) {
+        uint32_t lo, hi;
+        if (full) {
+            lo = pack16(__ldg(q + 2 * v));
+            hi = pack16(__ldg(q + 2 * v + 1));
+        } else {
+            uint32_t m2[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t cb = col0 + 32 * v + 16 * h;           // column of this chunk's byte 0
+                const int64_t lo_c = cb < 0 ? -cb : 0;
+                const int64_t hi_c = r - cb + 1;                      // valid bytes [lo_c, hi_c)
+                if (lo_c >= 16 || hi_c <= 0 || lo_c >= hi_c) {
+                    m2[h] = 0;
+                } else {
+                    // zero the bytes outside [lo_c, hi_c) BEFORE packing: pack16's multiply
+                    // is only collision-free for bytes in {0,1}, and bytes beyond the row
+                    // (or the buffer) may hold anything
+                    uint4 c = __ldg(q + 2 * v + h);
+                    uint32_t *cw = &c.x;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int lo = (int)(lo_c - 4 * u), hi = (int)(hi_c - 4 * u);
+                        const int l = lo < 0 ? 0 : (lo > 4 ? 4 : lo), g = hi < 0 ? 0 : (hi > 4 ? 4 : hi);
+                        const uint32_t mk = g <= l ? 0u : ((0xffffffffu >> (8 * (4 - g))) & (0xffffffffu << (8 * l)));
+                        cw[u] &= mk;
+                    }
+                    m2[h] = pack16(c);
+                }
+            }
+            lo = m2[0];
+            hi = m2[1];
+        }
+        const uint32_t P = lo | (hi << 16);               // stream bits [32v - e, 32v - e + 32)
+        if (v > 0) dst[v - 1] = __funnelshift_r(prev, P, e);
+        prev = P;
+    }
+}
+
+template <int RHO>
+__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem<RHO> &sm, uint32_t parity) {
+    constexpr int NIN = Cfg<RHO>::NIN, NW = Cfg<RHO>::NW, NT = Cfg<RHO>::NT, NBAND = Cfg<RHO>::NBAND;
+    const int t = threadIdx.x;
+    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
+    // ---- A: rows r0-1 .. r0+RHO -> bitmaps (one row per thread)
+    if constexpr (Stage<RHO>::kOn) {
+        phase_a_tma<RHO>(a, r0, c0, sm, parity);
+    } else {
+        (void)parity;
+        if (t < NIN) phase_a_row<RHO>(a, r0 - 1 + t, c0, sm.in[t]);
+    }
+    __syncthreads();
+    // ---- B: B3/S23 on words; thread = (word w, band of 8 output rows)
+    {
+        const int w = t % NW, band = t / NW;
+        constexpr int ROWS = RHO / NBAND;
+        const int y0 = band * ROWS;                       // first output row (in-row y0 + 1)
+        uint32_t h0u, h1u, p0m, p1m, Wm;                  // rolling: up row sums, mid pair sums
+        auto row_terms = [&](int yin, uint32_t &h0, uint32_t &h1, uint32_t &p0, uint32_t &p1, uint32_t &W) {
+            W = sm.in[yin][w];
+            const uint32_t Wp = w > 0 ? sm.in[yin][w - 1] : 0u;
+            const uint32_t Wn = w + 1 < NW ? sm.in[yin][w + 1] : 0u;
+            const uint32_t L = __funnelshift_l(Wp, W, 1);   // left neighbour of bit b = bit b-1
+            const uint32_t R = __funnelshift_r(W, Wn, 1);   // right neighbour
+            h0 = L ^ W ^ R;
+            h1 = (L & W) | (L & R) | (W & R);
+            p0 = L ^ R;
+            p1 = L & R;
+        };
+        uint32_t d0, d1, dp0, dp1, dW;
+        row_terms(y0, h0u, h1u, p0m, p1m, Wm);            // row above the band
+        uint32_t tmp0, tmp1;
+        row_terms(y0 + 1, tmp0, tmp1, p0m, p1m, Wm);      // first mid row
+        uint32_t h0m = tmp0, h1m = tmp1;
+#pragma unroll 1
+        for (int y = 0; y < ROWS; ++y) {
+            row_terms(y0 + y + 2, d0, d1, dp0, dp1, dW);  // row below
+            // nb = (h0u + 2 h1u) + (h0d + 2 h1d) + (p0m + 2 p1m); alive' <=> (nb | self) == 3
+            const uint32_t z0 = h0u ^ d0 ^ p0m;
+            const uint32_t k0 = (h0u & d0) | (h0u & p0m) | (d0 & p0m);
+            const uint32_t x = h1u ^ d1 ^ p1m;
+            const uint32_t ge2 = (h1u & d1) | (h1u & p1m) | (d1 & p1m);
+            const uint32_t one = ~ge2 & (x ^ k0);             // exactly one of {h1u, h1d, p1m, k0}
+            sm.out[y0 + y][w] = one & (z0 | Wm);
+            h0u = h0m; h1u = h1m;                             // mid becomes up
+            h0m = d0; h1m = d1; p0m = dp0; p1m = dp1; Wm = dW;
+        }
+    }
+    __syncthreads();
+    // ---- C: expand + aligned 16-byte stores; thread = (row, chunk slot)
+    constexpr int L = RHO / 16;                           // chunk slots per row
+#pragma unroll 1
+    for (int idx = t; idx < RHO * L; idx += NT) {
+        const int rr = idx / L, k = idx % L;
+        const int64_t i = r0 + rr;
+        if (i >= a.R1 || i < a.R0) continue;
+        uint64_t s;
+        if constexpr (Stage<RHO>::kOn) s = sm.seg[rr];        // computed once per row in phase A
+        else s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.base;
+        const int64_t seg = i - c0 + 1;
+        const int64_t len = seg < RHO ? seg : RHO;
+        const int off = (int)((0u - (uint32_t)s) & 15u) + 16 * k;
+        if (off >= len) continue;
+        const int64_t j0 = c0 + off;
+        if (j0 + 15 > i) {                                    // crosses the row end: SWAR edge path
+            ChunkPos p;
+            p.i = i; p.j0 = j0; p.c = s + (uint64_t)off; p.pm = nullptr; p.valid = true; p.fast = false;
+            chunk_general(a, p);
+            continue;
+        }
+        const int x = off + 1;                                // bitmap bit of column j0
+        const uint32_t w0 = sm.out[rr][x >> 5];
+        const uint32_t w1 = (x >> 5) + 1 < NW ? sm.out[rr][(x >> 5) + 1] : 0u;
+        const uint32_t b = __funnelshift_r(w0, w1, (uint32_t)(x & 31));
+        st_cs_v4u(a.out + s + (uint64_t)off, spread4(b & 15u), spread4((b >> 4) & 15u), spread4((b >> 8) & 15u),
+                  spread4((b >> 12) & 15u));
+    }
+}
+
+template <int RHO, int STRAT>
+__global__ void __launch_bounds__(Cfg<RHO>::NT) ca_bits_kernel(CaArgs a) {
+    __shared__ __align__(16) Smem<RHO> sm;
+    if (STRAT == TRI_BB) {
+        const uint32_t bj = blockIdx.x;
+        const uint32_t bi = blockIdx.y + (uint32_t)a.tile_row_begin;
+        if (bj > bi) return;
+    }
+    if constexpr (Stage<RHO>::kOn) {
+        if (threadIdx.x == 0) mbar_init(&sm.bar, Cfg<RHO>::NIN);
+        __syncthreads();
+    }
+    if (STRAT == TRI_BB) {
+        tile<RHO>(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm, 0u);
+    } else if (STRAT == TRI_LAMBDA) {
+        const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (w >= a.omega_end) return;
+        uint32_t bi, bj;
+        tri::lambda_map(w, bi, bj);
+        tile<RHO>(a, bi, bj, sm, 0u);
+    } else {
+        uint32_t parity = 0;
+#pragma unroll 1
+        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
+            uint32_t bi, bj;
+            tri::lambda_map(w, bi, bj);
+            tile<RHO>(a, bi, bj, sm, parity);
+            parity ^= 1u;
+            // generic-proxy reads of the staging buffer before the next tile's TMA writes
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();                                  // smem reused by the next tile
+        }
+    }
+}
+
+template <int RHO>
+tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+    constexpr int NT = Cfg<RHO>::NT;
+    if (strategy == TRI_BB) {
+        const int64_t tr0 = m.row_begin / m.rho;
+        const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;
+        if (tr1 <= tr0) return TRI_OK;
+        if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
+        a.tile_row_begin = tr0;
+        ca_bits_kernel<RHO, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
+    } else if (strategy == TRI_LAMBDA) {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        ca_bits_kernel<RHO, TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
+    } else {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_bits_kernel<RHO, TRI_LAMBDA_PERSIST>, NT, 0);
+        uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
+        if (g > nb) g = nb;
+        ca_bits_kernel<RHO, TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
+    }
+    tri::note_launches(1);
+    return tri::cuda_status();
+}
+
+}  // namespace bits
 
 constexpr int kCaThreads = 256;
 
@@ -253,8 +757,8 @@ tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_
     a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
     a.tile_row_begin = 0;
     switch (m.rho) {
-        case 128: return launch_r<128>(m, strategy, a, st);
-        case 256: return launch_r<256>(m, strategy, a, st);
+        case 128: return bits::launch<128>(m, strategy, a, st);    // bit-sliced tiles
+        case 256: return bits::launch<256>(m, strategy, a, st);
         case 512: return launch_r<512>(m, strategy, a, st);
         default: return TRI_EINVAL;
     }

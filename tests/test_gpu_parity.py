@@ -299,6 +299,26 @@ def test_ca_ranks_with_halos(orc, world):
     assert np.array_equal(ca_gpu(n, st, 5, "lambda", 128, world), orc.ca_run(n, st, 5))
 
 
+@pytest.mark.parametrize("rho", [128, 256, 512])
+@pytest.mark.parametrize("n", [1000, 2049])
+def test_ca_ignores_bytes_past_the_slice(orc, rho, n):
+    """State buffers embedded in 0xFF-filled allocations: whatever lies past the
+    packed slice (or past a row) must never leak into a cell."""
+    D = T(n)
+    st = inputs.ca_state(n, 7)
+    bigA = torch.full((D + 4096,), 255, dtype=torch.uint8, device="cuda")
+    bigB = torch.full((D + 4096,), 255, dtype=torch.uint8, device="cuda")
+    a, b = bigA[:D], bigB[:D]
+    a.copy_(torch.from_numpy(st))
+    m = tri.tri_map_init(n, rho)
+    for _ in range(3):
+        tri.tri_ca_step(m, "lambda", a, b)
+        a, b = b, a
+    sync()
+    assert np.array_equal(a.cpu().numpy(), orc.ca_run(n, st, 3))
+    assert (bigA[D:] == 255).all() and (bigB[D:] == 255).all()     # nothing written past the slice
+
+
 def test_ca_100_steps(orc):
     n = 2048
     st = inputs.ca_state(n, 7)
