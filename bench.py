@@ -264,6 +264,21 @@ def bench_dummy(pk):
         res[s + "_us"] = round(us, 3)
     res["I_lambda"] = round(res["bb_us"] / res["lambda_us"], 4)
     res["I_persist"] = round(res["bb_us"] / res["persist_us"], 4)
+    # section 4.1 / Fig. 2 on B200: the paper's uncorrected sqrt variants vs BB, and
+    # the first omega each variant gets wrong (GPU validity scan over omega < 2^26)
+    sq = {}
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for name, strat, var in (("lambda_X", "lambda_x", 1), ("lambda_N", "lambda_n", 2), ("lambda_R", "lambda_r", 3)):
+        us = 1e3 * graph_time(lambda s=strat: tri.tri_dummy(m, s, tri.TRI_DUMMY_PACKED, out), 100)
+        tri.tri_map_eval_variant(var, 0, 1 << 26, fail, first)
+        torch.cuda.synchronize()
+        sq[name] = {"us": round(us, 3), "I": round(res["bb_us"] / us, 4),
+                    "first_wrong_omega": int(first.item()) if fail.item() else None,
+                    "wrong_below_2^26": int(fail.item())}
+    sq["lambda (rsqrt + integer correction)"] = {"us": res["lambda_us"], "I": res["I_lambda"],
+                                                 "first_wrong_omega": None, "exact_to": "2^40"}
+    res["sqrt_variants"] = sq
     res["cells_per_s"] = T(n) / (min(res["lambda_us"], res["persist_us"]) * 1e-6)
     res["ctas"] = {"lambda": m.blocks, "bb": m.m * m.m}
     res["wasted_threads"] = {"lambda": m.waste_lambda, "bb": m.waste_bb}

@@ -46,6 +46,13 @@ typedef enum {
 } tri_status;
 
 enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2 };
+/* The paper's square-root variants of Eq. 4 (section 4.1), used WITHOUT
+ * the integer correction: lambda_X = IEEE sqrtf, lambda_N = 0x5f3759df seed + 3
+ * Newton steps + eps, lambda_R = x * rsqrtf(x) + eps, eps = 1e-4.  Exact only
+ * inside their validity range (see tri_map_eval_variant).  Accepted as a
+ * strategy by tri_dummy only (the map-cost experiment of Fig. 2). */
+enum { TRI_LAMBDA_X = 3, TRI_LAMBDA_N = 4, TRI_LAMBDA_R = 5 };
+enum { TRI_SQRT_X = 1, TRI_SQRT_N = 2, TRI_SQRT_R = 3 };
 enum { TRI_DUMMY_FIXED = 0, TRI_DUMMY_PACKED = 1, TRI_DUMMY_DIGEST = 2, TRI_DUMMY_COUNT = 3 };
 
 /* Exactness bound of the device lambda: omega < 2^40 (checked exhaustively). */
@@ -101,6 +108,15 @@ tri_status tri_lambda(uint64_t omega, uint32_t *bi, uint32_t *bj);
  * ERANGE: omega0 + count > 2^40. */
 tri_status tri_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ij,
                         unsigned long long *d_fail, void *stream);
+
+/* Validity scan of a square-root variant (TRI_SQRT_X / _N / _R) on omega in
+ * [omega0, omega0 + count): *d_fail (u64, zeroed by the call) = number of omega
+ * whose uncorrected variant differs from the exact lambda; *d_first (u64, set to
+ * UINT64_MAX by the call) = smallest such omega.  Reproduces the paper's
+ * "valid in N in [0, 30720]" claim on this hardware.
+ * EINVAL: bad variant; ERANGE: omega0 + count > 2^40. */
+tri_status tri_map_eval_variant(int32_t variant, uint64_t omega0, uint64_t count,
+                                unsigned long long *d_fail, unsigned long long *d_first, void *stream);
 
 /* Dummy kernel: each useful thread maps itself to (i,j).
  *   FIXED  : writes i + j to d_out[0] (u32; racy by design)

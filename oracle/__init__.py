@@ -66,6 +66,7 @@ def lib():
         L.orc_triplet_abs.argtypes = [i64, vp, ctypes.c_double, i64, i64, vp]
         L.orc_triplet_total.argtypes = [i64, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_variant_scan.argtypes = [i32, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]
         _lib = L
     return _lib
 
@@ -129,6 +130,14 @@ def tet_lam(omega: int):
     i, j, k = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
     _check(lib().orc_tet_lambda(omega, ctypes.byref(i), ctypes.byref(j), ctypes.byref(k)))
     return i.value, j.value, k.value
+
+
+def variant_scan(variant: int, w0: int, count: int):
+    """Section 4.1 sqrt variants (1 = lambda_X, 2 = lambda_N), uncorrected:
+    (number of omega in [w0, w0+count) they get wrong, first such omega or None)."""
+    f, first = u64(), u64()
+    _check(lib().orc_variant_scan(variant, w0, count, ctypes.byref(f), ctypes.byref(first)))
+    return f.value, (None if first.value == 2**64 - 1 else first.value)
 
 
 # --- dummy ----------------------------------------------------------------

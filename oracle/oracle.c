@@ -414,6 +414,59 @@ int orc_triplet_total(int64_t n, const float *pts, double nu, double *total)
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Square-root variants of Eq. 4 (section 4.1), uncorrected:       */
+/*   x = 1/4 + 2 w (fp32), s = sqrt(x) by the variant, i = floor(s - 1/2)      */
+/*   variant 1 (lambda_X): s = sqrtf(x) */
+/*   variant 2 (lambda_N): y0 = bits(0x5f3759df - (bits(x) >> 1)), three      */
+/*     Newton steps y = y (1.5 - (x/2) y^2), s = x y + 1e-4 */
+/* every operation IEEE fp32 round-to-nearest in this order (no contraction).  */
+/* lambda_R (hardware rsqrt) has no CPU definition: parity unpinned.           */
+/* The variant is correct at w iff T(i) <= w < T(i+1) (Eq. 3).      */
+/* Returns the number of failures in [w0, w0+count) and the first failing w    */
+/* (UINT64_MAX if none).                                                       */
+/* ------------------------------------------------------------------------ */
+static uint32_t variant_row(uint64_t w, int variant)
+{
+    float x = 0.25f + 2.0f * (float)w;
+    float s;
+    if (variant == 1) {
+        s = sqrtf(x);
+    } else {
+        float xh = 0.5f * x, y;
+        int32_t bits;
+        memcpy(&bits, &x, 4);
+        bits = 0x5f3759df - (bits >> 1);
+        memcpy(&y, &bits, 4);
+        for (int it = 0; it < 3; ++it) {
+            float yy = y * y;
+            float t = xh * yy;
+            float u = 1.5f - t;
+            y = y * u;
+        }
+        float xy = x * y;
+        s = xy + 1e-4f;
+    }
+    float f = floorf(s - 0.5f);
+    return f > 0.0f ? (uint32_t)f : 0u;
+}
+
+int orc_variant_scan(int32_t variant, uint64_t w0, uint64_t count, uint64_t *fails, uint64_t *first)
+{
+    if (variant != 1 && variant != 2) return ORC_EINVAL;
+    uint64_t nf = 0, fw = UINT64_MAX;
+    #pragma omp parallel for schedule(static) reduction(+:nf) reduction(min:fw)
+    for (uint64_t t = 0; t < count; ++t) {
+        uint64_t w = w0 + t;
+        uint64_t i = variant_row(w, variant);
+        int ok = (T2(i) <= w) && (w < T2(i + 1));
+        if (!ok) { nf += 1; if (w < fw) fw = w; }
+    }
+    *fails = nf;
+    *first = fw;
+    return ORC_OK;
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP

@@ -100,6 +100,14 @@ tri_status tri_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ij, unsigne
     return launch_map_eval(omega0, count, d_ij, d_fail, (cudaStream_t)stream);
 }
 
+tri_status tri_map_eval_variant(int32_t variant, uint64_t omega0, uint64_t count, unsigned long long *d_fail,
+                                unsigned long long *d_first, void *stream) {
+    g_launches = 0;
+    if (!d_fail || !d_first || variant < TRI_SQRT_X || variant > TRI_SQRT_R) return TRI_EINVAL;
+    if (omega0 > TRI_OMEGA_MAX || count > TRI_OMEGA_MAX - omega0) return TRI_ERANGE;
+    return launch_variant_scan(variant, omega0, count, d_fail, d_first, (cudaStream_t)stream);
+}
+
 static bool bad_strategy(int32_t s) { return s != TRI_LAMBDA && s != TRI_BB && s != TRI_LAMBDA_PERSIST; }
 
 static bool bad_map(const tri_map_t *m) {
@@ -112,7 +120,8 @@ static bool bad_map(const tri_map_t *m) {
 tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode, void *d_out,
                      size_t out_bytes, void *stream) {
     g_launches = 0;
-    if (bad_map(map) || bad_strategy(strategy) || !d_out) return TRI_EINVAL;
+    const bool variant = strategy >= TRI_LAMBDA_X && strategy <= TRI_LAMBDA_R;
+    if (bad_map(map) || (bad_strategy(strategy) && !variant) || !d_out) return TRI_EINVAL;
     if (map->rho != 8 && map->rho != 16 && map->rho != 32) return TRI_EINVAL;
     size_t need = 0;
     switch (mode) {

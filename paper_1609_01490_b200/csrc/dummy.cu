@@ -80,6 +80,15 @@ __global__ void __launch_bounds__(RHO * RHO) dummy_kernel(DummyArgs a) {
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
         dummy_body<RHO, MODE>(a, bi, bj, &acc);
+    } else if (STRAT >= TRI_LAMBDA_X) {
+        // the paper's uncorrected sqrt variants (section 4.1): outside their
+        // validity range the tile is wrong; tiles outside the triangle are skipped
+        const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (w >= a.omega_end) return;
+        uint32_t bi, bj;
+        tri::lambda_variant(w, STRAT - TRI_LAMBDA_X + TRI_SQRT_X, bi, bj);
+        if (bj > bi || (int64_t)bi * RHO >= a.n) return;
+        dummy_body<RHO, MODE>(a, bi, bj, &acc);
     } else {  // persistent
         for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
             uint32_t bi, bj;
@@ -120,6 +129,15 @@ tri_status launch3(const tri_map_t &m, int strategy, DummyArgs a, cudaStream_t s
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
         dummy_kernel<RHO, MODE, TRI_LAMBDA><<<tri::tile_grid(nb), blk, 0, st>>>(a);
+    } else if (strategy >= TRI_LAMBDA_X) {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        if (strategy == TRI_LAMBDA_X)
+            dummy_kernel<RHO, MODE, TRI_LAMBDA_X><<<tri::tile_grid(nb), blk, 0, st>>>(a);
+        else if (strategy == TRI_LAMBDA_N)
+            dummy_kernel<RHO, MODE, TRI_LAMBDA_N><<<tri::tile_grid(nb), blk, 0, st>>>(a);
+        else
+            dummy_kernel<RHO, MODE, TRI_LAMBDA_R><<<tri::tile_grid(nb), blk, 0, st>>>(a);
     } else {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;

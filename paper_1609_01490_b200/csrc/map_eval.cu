@@ -55,6 +55,33 @@ __global__ void __launch_bounds__(256) tet_eval_kernel(uint64_t w0, uint64_t cou
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(fail, bad);
 }
 
+// Validity scan of a square-root variant (section 4.1): compare the uncorrected
+// variant with the exact map; count mismatches and keep the first failing omega.
+__global__ void __launch_bounds__(256) variant_scan_kernel(int variant, uint64_t w0, uint64_t count,
+                                                           unsigned long long *fail, unsigned long long *first) {
+    unsigned long long bad = 0, mine = ~0ull;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+        const uint64_t w = w0 + t;
+        uint32_t i, j, vi, vj;
+        tri::lambda_map(w, i, j);
+        tri::lambda_variant(w, variant, vi, vj);
+        if (vi != i || vj != j) {
+            ++bad;
+            if (w < mine) mine = w;
+        }
+    }
+    bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, mine, o);
+        mine = other < mine ? other : mine;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bad) atomicAdd(fail, bad);
+        if (mine != ~0ull) atomicMin(first, mine);
+    }
+}
+
 unsigned eval_grid(uint64_t count) {
     uint64_t want = (count + 255) / 256;
     uint64_t cap = (uint64_t)tri::sm_count() * 8ull * 16ull;
@@ -71,6 +98,16 @@ tri_status launch_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ij, unsigned
     if (cudaMemsetAsync(d_fail, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
     if (count == 0) return TRI_OK;
     map_eval_kernel<<<eval_grid(count), 256, 0, st>>>(w0, count, d_ij, d_fail);
+    note_launches(1);
+    return cuda_status();
+}
+
+tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
+                               unsigned long long *d_first, cudaStream_t st) {
+    if (cudaMemsetAsync(d_fail, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
+    if (cudaMemsetAsync(d_first, 0xff, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
+    if (count == 0) return TRI_OK;
+    variant_scan_kernel<<<eval_grid(count), 256, 0, st>>>(variant, w0, count, d_fail, d_first);
     note_launches(1);
     return cuda_status();
 }

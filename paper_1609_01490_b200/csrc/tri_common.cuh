@@ -42,6 +42,47 @@ TRI_HD void lambda_map(uint64_t w, uint32_t &bi, uint32_t &bj) {
     bj = (uint32_t)(w - t);
 }
 
+// The paper's three square-root variants of Eq. 4 (section 4.1),
+// WITHOUT the integer correction -- exact only inside their validity range.
+// Operations are explicit round-to-nearest intrinsics (no FMA contraction) so
+// lambda_X and lambda_N are bit-reproducible on the CPU; lambda_R uses the
+// hardware MUFU.RSQ approximation and is not.
+//   lambda_X: i = floor(sqrtf(1/4 + 2 w) - 1/2)
+//   lambda_N: sqrt by x * (0x5f3759df seed + 3 Newton steps) + eps
+//   lambda_R: sqrt by x * rsqrtf(x) + eps
+// eps = 1e-4.  Variant ids: TRI_SQRT_X / _N / _R (include/tri.h).
+
+TRI_HD float sqrt_variant(float x, int variant) {
+#ifdef __CUDA_ARCH__
+    if (variant == TRI_SQRT_X) return __fsqrt_rn(x);
+    if (variant == TRI_SQRT_R) return __fadd_rn(__fmul_rn(x, rsqrtf(x)), 1e-4f);
+    // lambda_N: Carmack / Lomont reciprocal square root, three Newton steps
+    const float xh = __fmul_rn(0.5f, x);
+    float y = __int_as_float(0x5f3759df - (__float_as_int(x) >> 1));
+#pragma unroll
+    for (int it = 0; it < 3; ++it) y = __fmul_rn(y, __fsub_rn(1.5f, __fmul_rn(xh, __fmul_rn(y, y))));
+    return __fadd_rn(__fmul_rn(x, y), 1e-4f);
+#else
+    (void)variant;
+    return sqrtf(x);
+#endif
+}
+
+// lambda with a sqrt variant, no correction: returns false if i would be negative.
+TRI_HD void lambda_variant(uint64_t w, int variant, uint32_t &bi, uint32_t &bj) {
+#ifdef __CUDA_ARCH__
+    const float x = __fadd_rn(0.25f, __fmul_rn(2.0f, __ull2float_rn(w)));
+    const float s = __fsub_rn(sqrt_variant(x, variant), 0.5f);
+#else
+    const float x = 0.25f + 2.0f * (float)w;
+    const float s = sqrt_variant(x, variant) - 0.5f;
+#endif
+    const float f = floorf(s);
+    const uint32_t i = f > 0.0f ? (uint32_t)f : 0u;
+    bi = i;
+    bj = (uint32_t)(w - T2(i));     // wraps when i is wrong: the self-check compares with exact lambda
+}
+
 // Tetrahedral map: k = largest layer with T3(k) <= omega from an
 // fp32 cube-root estimate of (6 omega) (the real root y = x + 1 of
 // y^3 - y = 6 omega, reading Q13) plus one integer correction
@@ -101,6 +142,8 @@ tri_status launch_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ij, unsigned
                            cudaStream_t st);
 tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk,
                                unsigned long long *d_fail, cudaStream_t st);
+tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
+                               unsigned long long *d_first, cudaStream_t st);
 tri_status launch_dummy(const tri_map_t &m, int strategy, int mode, void *d_out, cudaStream_t st);
 tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int dim, int64_t ld,
                       float *out, cudaStream_t st);

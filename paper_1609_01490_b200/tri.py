@@ -17,7 +17,10 @@ LIB_PATH = os.path.join(HERE, "libtri.so")
 TRI_OK, TRI_EINVAL, TRI_ERANGE, TRI_ECUDA, TRI_ENOTSUP = 0, -1, -2, -3, -4
 TRI_LAMBDA, TRI_BB, TRI_LAMBDA_PERSIST = 0, 1, 2
 TRI_DUMMY_FIXED, TRI_DUMMY_PACKED, TRI_DUMMY_DIGEST, TRI_DUMMY_COUNT = 0, 1, 2, 3
-STRATEGIES = {"lambda": TRI_LAMBDA, "bb": TRI_BB, "persist": TRI_LAMBDA_PERSIST}
+TRI_LAMBDA_X, TRI_LAMBDA_N, TRI_LAMBDA_R = 3, 4, 5          # tri_dummy only (section 4.1 variants)
+TRI_SQRT_X, TRI_SQRT_N, TRI_SQRT_R = 1, 2, 3
+STRATEGIES = {"lambda": TRI_LAMBDA, "bb": TRI_BB, "persist": TRI_LAMBDA_PERSIST,
+              "lambda_x": TRI_LAMBDA_X, "lambda_n": TRI_LAMBDA_N, "lambda_r": TRI_LAMBDA_R}
 
 c_u64, c_i64, c_i32, c_u32, c_vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p
 
@@ -58,6 +61,7 @@ SIGNATURES = {
     "tri_map_init": ([ctypes.POINTER(TriMap), c_i64, c_i32, c_i32, c_i32, c_i32, c_i32], c_i32),
     "tri_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
     "tri_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
+    "tri_map_eval_variant": ([c_i32, c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
     "tri_dummy": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, ctypes.c_size_t, c_vp], c_i32),
     "tri_edm": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp], c_i32),
     "tri_edm_host": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_i32, c_i64, c_vp, c_vp, ctypes.c_size_t,
@@ -134,6 +138,12 @@ def tri_lambda(omega):
 
 def tri_map_eval(omega0, count, d_ij, d_fail, stream=None):
     _ok(lib().tri_map_eval(omega0, count, _ptr(d_ij), _ptr(d_fail), _stream(stream)), "tri_map_eval")
+
+
+def tri_map_eval_variant(variant, omega0, count, d_fail, d_first, stream=None):
+    """Validity scan of a section-4.1 sqrt variant (TRI_SQRT_X / _N / _R)."""
+    _ok(lib().tri_map_eval_variant(variant, omega0, count, _ptr(d_fail), _ptr(d_first), _stream(stream)),
+        "tri_map_eval_variant")
 
 
 def tet_map_init(n, rho, rank=0, world=1) -> TetMap:

@@ -93,6 +93,37 @@ def test_tet_map_matches_enumeration_and_exhaustive(orc):
     assert total == 0
 
 
+# ============================================================== sqrt variants (section 4.1)
+@pytest.mark.parametrize("variant,count", [(1, 12_000_000), (2, 2_000_000)])
+def test_sqrt_variant_scan_matches_oracle(orc, variant, count):
+    """lambda_X / lambda_N are IEEE-deterministic: the GPU's uncorrected variant
+    fails at exactly the omegas the C oracle's fp32 restatement fails at."""
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_map_eval_variant(variant, 0, count, fail, first)
+    sync()
+    nf, fw = orc.variant_scan(variant, 0, count)
+    assert fail.item() == nf and first.item() == fw
+
+
+def test_sqrt_variant_r_runs_and_dummy_variants():
+    """lambda_R depends on MUFU.RSQ rounding (parity unpinned): the scan runs; inside
+    the first-failure bound the variant dummy kernels give the exact digest."""
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_map_eval_variant(tri.TRI_SQRT_R, 0, 1 << 24, fail, first)
+    sync()
+    first_r = first.item() if fail.item() else 1 << 62
+    n, rho = 2048, 16
+    m = tri.tri_map_init(n, rho)
+    assert m.blocks < 100_000 and m.blocks < first_r
+    for s in ("lambda_x", "lambda_n", "lambda_r"):
+        dig = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tri.tri_dummy(m, s, tri.TRI_DUMMY_DIGEST, dig)
+        sync()
+        assert dig.item() == (n - 1) * n * (n + 1) // 2
+
+
 # ============================================================== dummy
 @pytest.mark.parametrize("strategy", STRATS)
 @pytest.mark.parametrize("n,rho", [(1, 8), (2, 16), (5, 8), (100, 16), (2048, 16), (1000, 32), (333, 8)])

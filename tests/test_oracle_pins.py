@@ -395,3 +395,36 @@ def test_triplet_abs_scale(orc):
     assert np.all(a >= np.abs(e) - 1e-12 * a)
     col = np.array([[0, 0, 0, 0], [0.5, 0, 0, 0], [1.0, 0, 0, 0]], np.float32)
     np.testing.assert_allclose(orc.triplet_abs(col), -orc.triplet(col), rtol=1e-12)
+
+
+# ---------------------------------------------------------------- sqrt variants (section 4.1)
+def _np_variant_rows(w, variant):
+    """Independent numpy float32 restatement of lambda_X / lambda_N."""
+    f32 = np.float32
+    x = (f32(0.25) + f32(2.0) * w.astype(np.float32)).astype(np.float32)
+    if variant == 1:
+        s = np.sqrt(x)
+    else:
+        xh = (f32(0.5) * x).astype(np.float32)
+        y = (np.int32(0x5f3759df) - (x.view(np.int32) >> 1)).astype(np.int32).view(np.float32)
+        for _ in range(3):
+            y = (y * (f32(1.5) - xh * (y * y))).astype(np.float32)
+        s = (x * y + f32(1e-4)).astype(np.float32)
+    return np.maximum(np.floor((s - f32(0.5)).astype(np.float32)), 0).astype(np.int64)
+
+
+@pytest.mark.parametrize("variant,lo,hi", [(1, 0, 12_000_000), (2, 0, 2_000_000)])
+def test_sqrt_variant_scan_vs_numpy(orc, variant, lo, hi):
+    first = None
+    fails = 0
+    for a in range(lo, hi, 1 << 20):
+        w = np.arange(a, min(hi, a + (1 << 20)), dtype=np.int64)
+        i = _np_variant_rows(w, variant)
+        bad = ~((i * (i + 1) // 2 <= w) & (w < (i + 1) * (i + 2) // 2))      # Eq. 3
+        fails += int(bad.sum())
+        if first is None and bad.any():
+            first = int(w[np.argmax(bad)])
+    got = orc.variant_scan(variant, lo, hi - lo)
+    assert got == (fails, first)
+    assert first is not None            # both variants do fail inside these ranges ...
+    assert first > 100_000              # ... but only after many exact rows (P:355-357)
