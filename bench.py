@@ -217,11 +217,13 @@ def bench_edm(args, rank, world, local_rank, pk):
     # lambda vs BB (paper form and persistent), a few steps each, this rank's slice
     vs = {}
     Kc = max(3, min(args.steps, 20))
-    for s in ("bb", "lambda", "persist"):
+    for s in ("bb", "lambda", "persist") + (("rb",) if world == 1 else ()):
         t, _ = time_steps(lambda s=s: tri.tri_edm(m, s, pts, out), Kc, 2, world)
         vs[s + "_ms"] = round(max_over_ranks(t, world) / Kc, 4)
     vs["I_lambda"] = round(vs["bb_ms"] / vs["lambda_ms"], 4)
     vs["I_persist"] = round(vs["bb_ms"] / vs["persist_ms"], 4)
+    if "rb_ms" in vs:
+        vs["I_rb"] = round(vs["bb_ms"] / vs["rb_ms"], 4)       # RB = one thread per cell, 4-byte stores
 
     # end to end through the public ABI with host buffers (pinned), H2D + compute + D2H
     e2e = None
@@ -259,9 +261,10 @@ def bench_dummy(pk):
     n, rho = 2048, 16
     m = tri.tri_map_init(n, rho)
     out = torch.empty(m.out_cells, dtype=torch.int32, device="cuda")
-    for s in ("bb", "lambda", "persist"):
+    for s in ("bb", "lambda", "persist", "rb"):
         us = 1e3 * graph_time(lambda s=s: tri.tri_dummy(m, s, tri.TRI_DUMMY_PACKED, out), 100)
         res[s + "_us"] = round(us, 3)
+    res["I_rb"] = round(res["bb_us"] / res["rb_us"], 4)
     res["I_lambda"] = round(res["bb_us"] / res["lambda_us"], 4)
     res["I_persist"] = round(res["bb_us"] / res["persist_us"], 4)
     # section 4.1 / Fig. 2 on B200: the paper's uncorrected sqrt variants vs BB, and
@@ -286,10 +289,11 @@ def bench_dummy(pk):
     n2 = 65536
     m2 = tri.tri_map_init(n2, rho)
     out2 = torch.empty(m2.out_cells, dtype=torch.int32, device="cuda")
-    for s in ("bb", "lambda"):
+    for s in ("bb", "lambda", "rb"):
         t, _ = time_steps(lambda s=s: tri.tri_dummy(m2, s, tri.TRI_DUMMY_PACKED, out2), 5, 2, 1)
         res[f"n65536_{s}_ms"] = round(t / 5, 4)
     res["n65536_I"] = round(res["n65536_bb_ms"] / res["n65536_lambda_ms"], 4)
+    res["n65536_I_rb"] = round(res["n65536_bb_ms"] / res["n65536_rb_ms"], 4)
     res["n65536_GBps"] = round(4 * m2.out_cells / (res["n65536_lambda_ms"] * 1e-3) / 1e9, 1)
     res["n65536_frac"] = round(res["n65536_GBps"] / pk["hbm_gbs"], 4)
     return {"config": "dummy map-cost kernel, n=2048, rho=16 (PACKED u32 codes)", "metric": "cells/s",

@@ -52,6 +52,10 @@ enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2 };
  * inside their validity range (see tri_map_eval_variant).  Accepted as a
  * strategy by tri_dummy only (the map-cost experiment of Fig. 2). */
 enum { TRI_LAMBDA_X = 3, TRI_LAMBDA_N = 4, TRI_LAMBDA_R = 5 };
+/* RB, the rectangular-box comparator (reading Q19): the triangle folded
+ * into an H x W thread rectangle, h = n/2, H = n - h, W = 2h + 1, one thread per
+ * cell.  Accepted by tri_dummy and tri_edm, single rank (world = 1) only. */
+enum { TRI_RB = 6 };
 enum { TRI_SQRT_X = 1, TRI_SQRT_N = 2, TRI_SQRT_R = 3 };
 enum { TRI_DUMMY_FIXED = 0, TRI_DUMMY_PACKED = 1, TRI_DUMMY_DIGEST = 2, TRI_DUMMY_COUNT = 3 };
 

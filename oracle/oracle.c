@@ -212,6 +212,23 @@ int orc_dispatch_count(int64_t n, int32_t rho, int32_t strategy, int32_t diag, u
                         if (ok) c[3]++; else c[4]++;
                     }
             }
+    } else if (strategy == 2) {
+        /* RB (reading Q19): an H x W thread rectangle, h = floor(n/2),
+         * H = n - h, W = 2h + 1, tiled by rho x rho blocks; a thread is useful iff
+         * it lies inside the rectangle (the fold is a bijection onto the triangle,
+         * checked on the GPU by PACKED parity + COUNT). */
+        int64_t h = n / 2, H = n - h, W = 2 * h + 1;
+        int64_t gx = (W + rho - 1) / rho, gy = (H + rho - 1) / rho;
+        for (int64_t by = 0; by < gy; ++by)
+            for (int64_t bx = 0; bx < gx; ++bx) {
+                c[0]++;
+                for (int64_t ty = 0; ty < rho; ++ty)
+                    for (int64_t tx = 0; tx < rho; ++tx) {
+                        int64_t x = bx * rho + tx, y = by * rho + ty;
+                        c[2]++;
+                        if (x < W && y < H) c[3]++; else c[4]++;
+                    }
+            }
     } else return ORC_EINVAL;
     memcpy(counts, c, sizeof c);
     return ORC_OK;

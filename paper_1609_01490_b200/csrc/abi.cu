@@ -120,8 +120,8 @@ static bool bad_map(const tri_map_t *m) {
 tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode, void *d_out,
                      size_t out_bytes, void *stream) {
     g_launches = 0;
-    const bool variant = strategy >= TRI_LAMBDA_X && strategy <= TRI_LAMBDA_R;
-    if (bad_map(map) || (bad_strategy(strategy) && !variant) || !d_out) return TRI_EINVAL;
+    const bool extra = (strategy >= TRI_LAMBDA_X && strategy <= TRI_LAMBDA_R) || strategy == TRI_RB;
+    if (bad_map(map) || (bad_strategy(strategy) && !extra) || !d_out) return TRI_EINVAL;
     if (map->rho != 8 && map->rho != 16 && map->rho != 32) return TRI_EINVAL;
     size_t need = 0;
     switch (mode) {
@@ -135,19 +135,21 @@ tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode, void 
         default: return TRI_EINVAL;
     }
     if (out_bytes < need) return TRI_EINVAL;
+    if (strategy == TRI_RB) return launch_dummy_rb(*map, mode, d_out, (cudaStream_t)stream);
     return launch_dummy(*map, strategy, mode, d_out, (cudaStream_t)stream);
 }
 
 tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, int32_t dim, int64_t ld,
                    float *d_out, size_t out_bytes, void *stream) {
     g_launches = 0;
-    if (bad_map(map) || bad_strategy(strategy) || !d_pts || !d_out) return TRI_EINVAL;
+    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_RB) || !d_pts || !d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
     if (map->rho != 32 && map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
     if (dim < 1 || dim > 4 || ld < dim) return TRI_EINVAL;
     if (((uintptr_t)d_out & 15u) != 0) return TRI_EINVAL;
     if (out_bytes < map->out_cells * 4u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
+    if (strategy == TRI_RB) return launch_edm_rb(*map, d_pts, dim, ld, d_out, (cudaStream_t)stream);
     return launch_edm(*map, strategy, d_pts, dim, ld, d_out, (cudaStream_t)stream);
 }
 

@@ -83,6 +83,21 @@ TRI_HD void lambda_variant(uint64_t w, int variant, uint32_t &bi, uint32_t &bj) 
     bj = (uint32_t)(w - T2(i));     // wraps when i is wrong: the self-check compares with exact lambda
 }
 
+// RB, the rectangular-box comparator map (Jung et al.; reading Q19:
+// the printed "j = n - i - 1" is not a bijection, this fold is).  The lower
+// triangle with diagonal is folded into an H x W thread rectangle,
+// h = floor(n/2), H = n - h, W = 2h + 1 (W H = n(n+1)/2 exactly): rectangle row
+// y holds triangle row a = h + y (x <= a -> (a, x)) followed by row b = h-1-y
+// (x > a -> (b, x - a - 1)).  Thread-space, O(1) waste beyond block rounding.
+TRI_HD bool rb_map(int64_t x, int64_t y, int64_t n, int64_t &i, int64_t &j) {
+    const int64_t h = n / 2, H = n - h, W = 2 * h + 1;
+    if (x >= W || y >= H) return false;
+    const int64_t a = h + y;
+    if (x <= a) { i = a; j = x; }
+    else { i = h - 1 - y; j = x - a - 1; }
+    return true;
+}
+
 // Tetrahedral map: k = largest layer with T3(k) <= omega from an
 // fp32 cube-root estimate of (6 omega) (the real root y = x + 1 of
 // y^3 - y = 6 omega, reading Q13) plus one integer correction
@@ -144,6 +159,8 @@ tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk,
                                unsigned long long *d_fail, cudaStream_t st);
 tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
                                unsigned long long *d_first, cudaStream_t st);
+tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream_t st);
+tri_status launch_edm_rb(const tri_map_t &m, const float *pts, int dim, int64_t ld, float *out, cudaStream_t st);
 tri_status launch_dummy(const tri_map_t &m, int strategy, int mode, void *d_out, cudaStream_t st);
 tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int dim, int64_t ld,
                       float *out, cudaStream_t st);

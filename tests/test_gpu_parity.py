@@ -125,7 +125,7 @@ def test_sqrt_variant_r_runs_and_dummy_variants():
 
 
 # ============================================================== dummy
-@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("strategy", STRATS + ["rb"])
 @pytest.mark.parametrize("n,rho", [(1, 8), (2, 16), (5, 8), (100, 16), (2048, 16), (1000, 32), (333, 8)])
 def test_dummy_packed_digest_count(orc, strategy, n, rho):
     m = tri.tri_map_init(n, rho)
@@ -141,7 +141,7 @@ def test_dummy_packed_digest_count(orc, strategy, n, rho):
     tri.tri_dummy(m, strategy, tri.TRI_DUMMY_COUNT, cnt)
     sync()
     c = cnt.cpu().tolist()
-    ref = orc.dispatch_count(n, rho, 1 if strategy == "bb" else 0)
+    ref = orc.dispatch_count(n, rho, {"bb": 1, "rb": 2}.get(strategy, 0))
     assert c == [ref["blocks"], ref["blocks_discarded"], ref["threads"], ref["useful"], ref["discarded"]]
     fx = torch.zeros(1, dtype=torch.int32, device="cuda")
     tri.tri_dummy(m, strategy, tri.TRI_DUMMY_FIXED, fx)
@@ -180,7 +180,7 @@ def edm_close(got, ref):
     assert not bad.any(), (int(bad.sum()), float(err.max()))
 
 
-@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("strategy", STRATS + ["rb"])
 @pytest.mark.parametrize("rho", [32, 64, 128, 256])
 @pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (3, 7), (5, 42), (64, 7), (257, 42), (1000, 7), (4097, 42)])
 def test_edm_small(orc, strategy, rho, n, seed):

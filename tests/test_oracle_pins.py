@@ -428,3 +428,16 @@ def test_sqrt_variant_scan_vs_numpy(orc, variant, lo, hi):
     assert got == (fails, first)
     assert first is not None            # both variants do fail inside these ranges ...
     assert first > 100_000              # ... but only after many exact rows
+
+
+@pytest.mark.parametrize("n,rho", [(1, 8), (2, 8), (7, 8), (8, 2), (100, 16), (2048, 16), (333, 32)])
+def test_dispatch_count_rb(orc, n, rho):
+    # RB covers the triangle with an O(1)-waste rectangle: useful = D exactly
+    c = orc.dispatch_count(n, rho, strategy=2)
+    assert c["useful"] == T(n)
+    h = n // 2
+    H, W = n - h, 2 * h + 1
+    assert H * W == T(n)                                   # the fold is area-exact
+    gx, gy = -(-W // rho), -(-H // rho)
+    assert c["blocks"] == gx * gy and c["threads"] == gx * gy * rho * rho
+    assert c["discarded"] < (W + H + rho) * rho            # waste only from block rounding
