@@ -175,6 +175,19 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
                        uint8_t *d_out, const uint8_t *d_halo_above,
                        const uint8_t *d_halo_below, void *d_ws, void *stream);
 
+/* k generations of the same rule in one call (temporal blocking, deep halos;
+ * k in 1..8, rho = 128): d_out = the state after k generations of the whole
+ * domain restricted to this rank's slice, given the current state of the
+ * rank's rows (d_in) and of the k rows on either side.  d_halo_above = the
+ * packed rows [max(row_begin - k, 0), row_begin) (contiguous in the owner's
+ * slice) or NULL when row_begin == 0; d_halo_below = the packed rows
+ * [row_end, min(row_end + k, n)) or NULL when row_end == n.  Each tile writes
+ * only its own cells (partial 16-byte chunks byte-wise).  k = 1 computes the
+ * same result as tri_ca_step.  HBM traffic per cell-generation ~2.2/k bytes. */
+tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in,
+                        uint8_t *d_out, const uint8_t *d_halo_above, const uint8_t *d_halo_below,
+                        void *d_ws, void *stream);
+
 /*
  * Tetrahedral map descriptor.  Tiles (i, j, k), j <= i <= k < m,
  * enumerated layer-major (layer k = a triangle of side k+1, Eq. 1 inside).

@@ -180,6 +180,18 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
     return launch_ca(*map, strategy, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);
 }
 
+tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in, uint8_t *d_out,
+                        const uint8_t *d_halo_above, const uint8_t *d_halo_below, void *d_ws, void *stream) {
+    g_launches = 0;
+    (void)d_ws;
+    if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
+    if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
+    if (map->rho != 128 || k < 1 || k > 8) return TRI_EINVAL;
+    if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
+    if (map->out_cells == 0) return TRI_OK;
+    return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);
+}
+
 tri_status tet_map_init(tet_map_t *map, int64_t n, int32_t rho, int32_t rank, int32_t world) {
     if (!map || n < 3 || (rho != 4 && rho != 8 && rho != 16 && rho != 32) || world < 1 || rank < 0 ||
         rank >= world)

@@ -26,9 +26,11 @@ namespace {
 struct CaArgs {
     const uint8_t *in;
     uint8_t *out;
-    const uint8_t *above, *below;  // halo rows R0-1 and R1 (NULL = dead)
+    const uint8_t *above, *below;  // halo rows [R0-k, R0) and [R1, R1+k), packed (NULL = dead)
     int64_t n, R0, R1;             // this slice owns rows [R0, R1)
+    int64_t k;                     // halo depth (generations per launch)
     uint64_t base;                 // T(R0)
+    uint64_t above_base;           // T(max(R0 - k, 0)): packed start of the above block
     uint64_t out_cells;
     uint64_t omega_begin, omega_end;
     int64_t tile_row_begin;
@@ -37,8 +39,9 @@ struct CaArgs {
 // Row pointer to column 0 of row r, or nullptr for a dead row.
 __device__ __forceinline__ const uint8_t *row_ptr(const CaArgs &a, int64_t r) {
     if (r < 0 || r >= a.n) return nullptr;
-    if (r < a.R0) return (r == a.R0 - 1) ? a.above : nullptr;
-    if (r >= a.R1) return (r == a.R1) ? a.below : nullptr;
+    if (r < a.R0) return (r >= a.R0 - a.k && a.above) ? a.above + (tri::T2((uint64_t)r) - a.above_base) : nullptr;
+    if (r >= a.R1)
+        return (r < a.R1 + a.k && a.below) ? a.below + (tri::T2((uint64_t)r) - tri::T2((uint64_t)a.R1)) : nullptr;
     return a.in + (tri::T2((uint64_t)r) - a.base);
 }
 
@@ -690,6 +693,252 @@ tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
 
 }  // namespace bits
 
+// ============================================================================
+// k generations per launch (temporal blocking with deep halos):
+// rho = 128 tiles; the CTA stages rows [r0-k, r0+rho+k) x columns
+// [c0-k, c0+rho+k) (TMA bulk copies), packs them to bitmaps, runs k
+// generations in shared memory -- re-masking the triangle after each one --
+// and writes only its own row segments [c0, min(c0+rho, i+1)): aligned chunks
+// with 16-byte streaming stores, the partial chunks at segment ends byte-wise
+// (a neighbouring tile writes the other bytes of such a chunk).  Garbage from
+// the region edge moves one cell per generation, so after k generations the
+// central rho x rho block is exact.  HBM traffic per cell-generation falls from
+// 2 bytes to about (1.2 + 1) / k bytes.
+namespace multi {
+
+constexpr int RHO = 128;
+constexpr int KMAX = 8;
+constexpr int NINMAX = RHO + 2 * KMAX;   // input rows
+constexpr int NW = 5;                    // bitmap words per row: bit x <-> column c0 - k + x (rho + 2k <= 160)
+constexpr int NT = 32 * NW;              // 160 threads: phase B = NW words x 32 bands
+constexpr int RAWB = 32 * (NW + 1);      // staged bytes per row (>= 15 + rho + 2k)
+constexpr int NCH = RAWB / 16;
+constexpr int STRIDE = RAWB + 16;        // 16 (mod 128): conflict-free LDS.128 across rows
+constexpr int SLOTS = RHO / 16 + 1;      // 16-byte chunks a row segment can touch
+
+struct Smem {
+    uint32_t A[NINMAX][NW], B[NINMAX][NW], M[NINMAX][NW];   // ping-pong bitmaps, triangle masks
+    alignas(16) uint8_t raw[NINMAX][STRIDE];
+    uint64_t seg[RHO];
+    alignas(8) unsigned long long bar;
+};
+
+// bits of columns [cb, cb + 32) that lie inside row r of the triangle
+__device__ __forceinline__ uint32_t tri_mask(int64_t r, int64_t n, int64_t cb) {
+    if (r < 0 || r >= n) return 0u;
+    const int64_t lo = cb < 0 ? -cb : 0;              // first valid bit
+    const int64_t hi = r - cb + 1;                    // one past the last valid bit
+    if (hi <= 0 || lo >= 32 || lo >= hi) return 0u;
+    const uint32_t up = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+    return up & ~((1u << lo) - 1u);
+}
+
+__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm, uint32_t parity) {
+    const int t = threadIdx.x;
+    const int K = (int)a.k;
+    const int NIN = RHO + 2 * K;
+    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
+    const int64_t cs = c0 - K;                        // column of bitmap bit 0
+    // ---- A: stage + pack rows r0-K .. r0+RHO+K-1 (thread t = input row t)
+    if (t < NINMAX) {
+        if (t < NIN) {
+            const int64_t r = r0 - K + t;
+            if (t >= K && t < K + RHO) sm.seg[t - K] = tri::T2((uint64_t)r) + (uint64_t)c0 - a.base;
+            uint8_t *dst = sm.raw[t];
+            const uint8_t *p = row_ptr(a, r);
+            uint32_t e = 0;
+            if (!p) {
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) *reinterpret_cast<uint4 *>(dst + 16 * h) = make_uint4(0, 0, 0, 0);
+                bits::mbar_arrive(&sm.bar);
+            } else {
+                const uintptr_t Ad = (uintptr_t)(p + cs);
+                e = (uint32_t)(Ad & 15u);
+                const int64_t col0 = cs - (int64_t)e;
+                const uint4 *q = (const uint4 *)(Ad & ~(uintptr_t)15);
+                if (col0 >= 0 && col0 + RAWB - 1 <= r) {
+                    bits::mbar_arrive_tx(&sm.bar, RAWB);
+                    bits::bulk_g2s(dst, q, RAWB, &sm.bar);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h) {
+                        const int64_t cb = col0 + 16 * h;
+                        const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
+                        uint4 c = make_uint4(0, 0, 0, 0);
+                        if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
+                            c = __ldg(q + h);
+                            bits::mask_chunk(c, lo_c, hi_c);
+                        }
+                        *reinterpret_cast<uint4 *>(dst + 16 * h) = c;
+                    }
+                    bits::mbar_arrive(&sm.bar);
+                }
+            }
+            bits::mbar_wait(&sm.bar, parity);
+            uint32_t prev = 0;
+#pragma unroll
+            for (int v = 0; v <= NW; ++v) {
+                const uint32_t lo = bits::pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v));
+                const uint32_t hi = bits::pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v + 16));
+                const uint32_t P = lo | (hi << 16);
+                if (v > 0) {
+                    const uint32_t mk = tri_mask(r, a.n, cs + 32 * (v - 1));
+                    sm.M[t][v - 1] = mk;
+                    sm.A[t][v - 1] = __funnelshift_r(prev, P, e) & mk;
+                }
+                prev = P;
+            }
+        } else {
+            // rows the mbarrier counts but this K does not use
+            bits::mbar_arrive(&sm.bar);
+        }
+    }
+    __syncthreads();
+    // ---- B: K generations, ping-pong A -> B -> A ...
+    const int w = t % NW, band = t / NW;
+#pragma unroll 1
+    for (int g = 1; g <= K; ++g) {
+        uint32_t (*src)[NW] = (g & 1) ? sm.A : sm.B;
+        uint32_t (*dst)[NW] = (g & 1) ? sm.B : sm.A;
+        const int y_lo = g, y_hi = NIN - g;                    // rows computed this generation
+        const int rows = (y_hi - y_lo + 31) / 32;
+        const int ya = y_lo + band * rows;
+        int yb = ya + rows;
+        if (yb > y_hi) yb = y_hi;
+        auto terms = [&](int y, uint32_t &h0, uint32_t &h1, uint32_t &p0, uint32_t &p1, uint32_t &W) {
+            W = src[y][w];
+            const uint32_t Wp = w > 0 ? src[y][w - 1] : 0u;
+            const uint32_t Wn = w + 1 < NW ? src[y][w + 1] : 0u;
+            const uint32_t L = __funnelshift_l(Wp, W, 1), R = __funnelshift_r(W, Wn, 1);
+            h0 = L ^ W ^ R;
+            h1 = (L & W) | (L & R) | (W & R);
+            p0 = L ^ R;
+            p1 = L & R;
+        };
+        if (ya < yb) {
+            uint32_t h0u, h1u, h0m, h1m, p0m, p1m, Wm, xx, yy;
+            terms(ya - 1, h0u, h1u, xx, yy, Wm);
+            terms(ya, h0m, h1m, p0m, p1m, Wm);
+#pragma unroll 1
+            for (int y = ya; y < yb; ++y) {
+                uint32_t d0, d1, dp0, dp1, dW;
+                terms(y + 1, d0, d1, dp0, dp1, dW);
+                const uint32_t z0 = h0u ^ d0 ^ p0m;
+                const uint32_t k0 = (h0u & d0) | (h0u & p0m) | (d0 & p0m);
+                const uint32_t x = h1u ^ d1 ^ p1m;
+                const uint32_t ge2 = (h1u & d1) | (h1u & p1m) | (d1 & p1m);
+                dst[y][w] = (~ge2 & (x ^ k0)) & (z0 | Wm) & sm.M[y][w];
+                h0u = h0m; h1u = h1m;
+                h0m = d0; h1m = d1; p0m = dp0; p1m = dp1; Wm = dW;
+            }
+        }
+        __syncthreads();
+    }
+    uint32_t (*fin)[NW] = (K & 1) ? sm.B : sm.A;
+    // ---- C: aligned-chunk ownership (a 16-byte chunk is written by the tile
+    // holding its first cell; the region covers the <= 15-column spill past the
+    // tile for K <= 8).  Byte stores only where a chunk crosses a row boundary:
+    // the row-i part of a chunk running past the row end (diagonal tiles), and
+    // the head bytes of a row whose first chunk started in the previous row (c0 = 0).
+    constexpr int L = RHO / 16;
+#pragma unroll 1
+    for (int idx = t; idx < RHO * SLOTS; idx += NT) {
+        const int rr = idx / SLOTS, q = idx % SLOTS;
+        const int64_t i = r0 + rr;
+        if (i >= a.R1 || i < a.R0) continue;
+        const int64_t seg = i - c0 + 1;
+        const int64_t len = seg < RHO ? seg : RHO;
+        if (len <= 0) continue;
+        const uint64_t s = sm.seg[rr];
+        const int delta = (int)((0u - (uint32_t)s) & 15u);
+        const int y = rr + K;
+        if (q == L) {                                          // head bytes of the row (c0 = 0 only)
+            if (c0 != 0) continue;
+            const int hb = delta < len ? delta : (int)len;
+#pragma unroll 1
+            for (int u = 0; u < hb; ++u) {
+                const int x = u + K;
+                a.out[s + u] = (uint8_t)((fin[y][x >> 5] >> (x & 31)) & 1u);
+            }
+            continue;
+        }
+        const int off = delta + 16 * q;
+        if (off >= len) continue;
+        const int64_t j0 = c0 + off;
+        const int x = off + K;
+        if (j0 + 15 <= i) {
+            const uint32_t w0 = fin[y][x >> 5];
+            const uint32_t w1 = (x >> 5) + 1 < NW ? fin[y][(x >> 5) + 1] : 0u;
+            const uint32_t b = __funnelshift_r(w0, w1, (uint32_t)(x & 31));
+            st_cs_v4u(a.out + s + off, bits::spread4(b & 15u), bits::spread4((b >> 4) & 15u),
+                      bits::spread4((b >> 8) & 15u), bits::spread4((b >> 12) & 15u));
+        } else {                                               // crosses the row end: row-i part only
+#pragma unroll 1
+            for (int u = 0; u <= (int)(i - j0); ++u) {
+                const int xu = x + u;
+                a.out[s + off + u] = (uint8_t)((fin[y][xu >> 5] >> (xu & 31)) & 1u);
+            }
+        }
+    }
+}
+
+template <int STRAT>
+__global__ void __launch_bounds__(NT) ca_multi_kernel(CaArgs a) {
+    __shared__ __align__(16) Smem sm;
+    if (STRAT == TRI_BB) {
+        if (blockIdx.x > blockIdx.y + (uint32_t)a.tile_row_begin) return;
+    }
+    if (threadIdx.x == 0) bits::mbar_init(&sm.bar, NINMAX);
+    __syncthreads();
+    if (STRAT == TRI_BB) {
+        tile(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm, 0u);
+    } else if (STRAT == TRI_LAMBDA) {
+        const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (w >= a.omega_end) return;
+        uint32_t bi, bj;
+        tri::lambda_map(w, bi, bj);
+        tile(a, bi, bj, sm, 0u);
+    } else {
+        uint32_t parity = 0;
+#pragma unroll 1
+        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
+            uint32_t bi, bj;
+            tri::lambda_map(w, bi, bj);
+            tile(a, bi, bj, sm, parity);
+            parity ^= 1u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+        }
+    }
+}
+
+tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+    if (strategy == TRI_BB) {
+        const int64_t tr0 = m.row_begin / m.rho;
+        const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;
+        if (tr1 <= tr0) return TRI_OK;
+        if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
+        a.tile_row_begin = tr0;
+        ca_multi_kernel<TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
+    } else if (strategy == TRI_LAMBDA) {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        ca_multi_kernel<TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
+    } else {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<TRI_LAMBDA_PERSIST>, NT, 0);
+        uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
+        if (g > nb) g = nb;
+        ca_multi_kernel<TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
+    }
+    tri::note_launches(1);
+    return tri::cuda_status();
+}
+
+}  // namespace multi
+
 constexpr int kCaThreads = 256;
 
 template <int RHO, int STRAT>
@@ -753,7 +1002,9 @@ tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_
     a.above = m.row_begin > 0 ? above : nullptr;
     a.below = m.row_end < m.n ? below : nullptr;
     a.n = m.n; a.R0 = m.row_begin; a.R1 = m.row_end;
+    a.k = 1;
     a.base = m.out_offset; a.out_cells = m.out_cells;
+    a.above_base = m.row_begin > 0 ? T2((uint64_t)m.row_begin - 1) : 0;
     a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
     a.tile_row_begin = 0;
     switch (m.rho) {
@@ -762,6 +1013,23 @@ tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_
         case 512: return launch_r<512>(m, strategy, a, st);
         default: return TRI_EINVAL;
     }
+}
+
+tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,
+                           const uint8_t *above, const uint8_t *below, cudaStream_t st) {
+    if (((uintptr_t)out & 15u) != 0 || ((uintptr_t)in & 15u) != 0) return TRI_EINVAL;
+    CaArgs a;
+    a.in = in; a.out = out;
+    a.above = m.row_begin > 0 ? above : nullptr;
+    a.below = m.row_end < m.n ? below : nullptr;
+    a.n = m.n; a.R0 = m.row_begin; a.R1 = m.row_end;
+    a.k = k;
+    a.base = m.out_offset; a.out_cells = m.out_cells;
+    const int64_t first_above = m.row_begin - k > 0 ? m.row_begin - k : 0;
+    a.above_base = T2((uint64_t)first_above);
+    a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
+    a.tile_row_begin = 0;
+    return multi::launch(m, strategy, a, st);
 }
 
 }  // namespace tri

@@ -160,6 +160,8 @@ tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk,
 tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
                                unsigned long long *d_first, cudaStream_t st);
 tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream_t st);
+tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,
+                           const uint8_t *above, const uint8_t *below, cudaStream_t st);
 tri_status launch_edm_rb(const tri_map_t &m, const float *pts, int dim, int64_t ld, float *out, cudaStream_t st);
 tri_status launch_dummy(const tri_map_t &m, int strategy, int mode, void *d_out, cudaStream_t st);
 tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int dim, int64_t ld,

@@ -59,27 +59,43 @@ def owner(bounds, r):
     return None
 
 
+def halo_bytes(bounds, n: int, rank: int, k: int = 1):
+    """Sizes of the packed halo blocks a rank receives: rows [R0-k, R0) and [R1, R1+k)."""
+    R0, R1 = bounds[rank]
+    a = T(R0) - T(max(R0 - k, 0))
+    b = T(min(R1 + k, n)) - T(R1)
+    return a, b
+
+
 def halo_exchange(state: torch.Tensor, bounds, n: int, rank: int, above: torch.Tensor | None,
-                  below: torch.Tensor | None):
+                  below: torch.Tensor | None, k: int = 1):
     """Exchange the CA boundary rows of this rank's packed slice ``state``.
 
     bounds[g] = (row_begin, row_end) of rank g (every rank computes the same
-    list from tri_map_init; no communication).  ``above`` receives row R0 - 1
-    (R0 bytes) and ``below`` receives row R1 (R1 + 1 bytes).  Rows are
-    contiguous in the packed Eq. 1 slice, so the sends are views.  Ranks that
-    own no rows take no part.
+    list from tri_map_init; no communication).  ``above`` receives the k packed
+    rows [R0-k, R0), ``below`` the k rows [R1, R1+k) (k = 1: the single
+    neighbour rows of tri_ca_step; k > 1: the deep halos of tri_ca_steps).
+    Rows are contiguous in the packed Eq. 1 slice, so the sends are views.
+    Ranks that own no rows take no part; a rank's k halo rows must all belong to
+    one neighbour (every non-empty rank owns >= k rows).
     """
     R0, R1 = bounds[rank]
     if R1 <= R0:
         return
     sends, recvs = [], []
-    if R0 > 0:                                   # my first row is the "below" halo of owner(R0-1)
-        sends.append((state[0:R0 + 1], owner(bounds, R0 - 1)))
-        recvs.append((above, owner(bounds, R0 - 1)))
-    if R1 < n:                                   # my last row is the "above" halo of owner(R1)
-        o = T(R1 - 1) - T(R0)
-        sends.append((state[o:o + R1], owner(bounds, R1)))
-        recvs.append((below, owner(bounds, R1)))
+    if R0 > 0:                                   # my first k rows are the "below" halo of owner(R0-1)
+        g = owner(bounds, R0 - 1)
+        if owner(bounds, max(R0 - k, 0)) != g:
+            raise ValueError("deep halo spans several ranks: every rank needs >= k rows")
+        sends.append((state[0:T(min(R0 + k, R1)) - T(R0)], g))
+        recvs.append((above, g))
+    if R1 < n:                                   # my last k rows are the "above" halo of owner(R1)
+        g = owner(bounds, R1)
+        if owner(bounds, min(R1 + k, n) - 1) != g:
+            raise ValueError("deep halo spans several ranks: every rank needs >= k rows")
+        first = max(R1 - k, R0)
+        sends.append((state[T(first) - T(R0):T(R1) - T(R0)], g))
+        recvs.append((below, g))
     if not sends:
         return
     staged = _gloo() and state.is_cuda

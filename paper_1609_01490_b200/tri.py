@@ -70,6 +70,7 @@ SIGNATURES = {
     "tri_collide": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_vp, c_vp], c_i32),
     "tri_ca_workspace_size": ([ctypes.POINTER(TriMap)], ctypes.c_size_t),
     "tri_ca_step": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_i32),
+    "tri_ca_steps": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_i32),
     "tet_map_init": ([ctypes.POINTER(TetMap), c_i64, c_i32, c_i32, c_i32], c_i32),
     "tet_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
     "tet_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
@@ -199,6 +200,13 @@ def tri_ca_step(m: TriMap, strategy, state_in, state_out, halo_above=None, halo_
                 stream=None):
     _ok(lib().tri_ca_step(ctypes.byref(m), _strategy(strategy), _ptr(state_in), _ptr(state_out),
                           _ptr(halo_above), _ptr(halo_below), _ptr(ws), _stream(stream)), "tri_ca_step")
+
+
+def tri_ca_steps(m: TriMap, strategy, k, state_in, state_out, halo_above=None, halo_below=None, ws=None,
+                 stream=None):
+    """k generations in one call; halos are the k packed rows on either side."""
+    _ok(lib().tri_ca_steps(ctypes.byref(m), _strategy(strategy), int(k), _ptr(state_in), _ptr(state_out),
+                           _ptr(halo_above), _ptr(halo_below), _ptr(ws), _stream(stream)), "tri_ca_steps")
 
 
 def tet_triplet(m: TetMap, strategy, pts4, energy, nu=1.0, stream=None):

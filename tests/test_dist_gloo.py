@@ -30,7 +30,7 @@ def _init(rank, world, port):
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
 
-def _ca_worker(rank, world, port, n, rho, steps, q):
+def _ca_worker(rank, world, port, n, rho, steps, q, k=1):
     try:
         _init(rank, world, port)
         import oracle
@@ -41,17 +41,22 @@ def _ca_worker(rank, world, port, n, rho, steps, q):
         full0 = inputs.ca_state(n, 42)
         state = torch.from_numpy(full0[m.out_offset:m.out_offset + m.out_cells].copy())
         R0, R1 = bounds[rank]
-        above = torch.zeros(max(R0, 1), dtype=torch.uint8)
-        below = torch.zeros(R1 + 1, dtype=torch.uint8)
+        na, nb = tdist.halo_bytes(bounds, n, rank, k)
+        above = torch.zeros(max(na, 1), dtype=torch.uint8)
+        below = torch.zeros(max(nb, 1), dtype=torch.uint8)
         for _ in range(steps):
-            tdist.halo_exchange(state, bounds, n, rank, above if R0 > 0 else None, below if R1 < n else None)
+            tdist.halo_exchange(state, bounds, n, rank, above if R0 > 0 else None, below if R1 < n else None, k)
             if R1 > R0:
+                # the rank's rows plus its k-deep halos, everything else dead; k
+                # generations of the oracle are exact on [R0, R1) (light cone)
                 work = np.zeros(T(n), np.uint8)
                 work[T(R0):T(R1)] = state.numpy()
                 if R0 > 0:
-                    work[T(R0 - 1):T(R0)] = above.numpy()[:R0]
+                    work[T(max(R0 - k, 0)):T(R0)] = above.numpy()[:na]
                 if R1 < n:
-                    work[T(R1):T(R1 + 1)] = below.numpy()
+                    work[T(R1):T(min(R1 + k, n))] = below.numpy()[:nb]
+                for _ in range(k - 1):
+                    work = oracle.ca_step(n, work)
                 state = torch.from_numpy(oracle.ca_step_rows(n, work, R0, R1).copy())
         parts = [None] * world
         dist.all_gather_object(parts, state.numpy().tobytes())
@@ -67,14 +72,15 @@ def _ca_worker(rank, world, port, n, rho, steps, q):
         raise
 
 
-@pytest.mark.parametrize("world,n,rho", [(2, 700, 128), (3, 1000, 128), (2, 300, 256)])
-def test_ca_halo_exchange_matches_oracle(orc, world, n, rho):
+@pytest.mark.parametrize("world,n,rho,k", [(2, 700, 128, 1), (3, 1000, 128, 1), (2, 300, 256, 1),
+                                           (3, 900, 128, 3), (2, 600, 128, 8)])
+def test_ca_halo_exchange_matches_oracle(orc, world, n, rho, k):
     from paper_1609_01490_b200 import inputs
-    steps = 4
+    steps = 4 if k == 1 else 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ca_worker, args=(g, world, port, n, rho, steps, q)) for g in range(world)]
+    procs = [ctx.Process(target=_ca_worker, args=(g, world, port, n, rho, steps, q, k)) for g in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=300)
@@ -83,6 +89,6 @@ def test_ca_halo_exchange_matches_oracle(orc, world, n, rho):
     assert not isinstance(res, str), res
     data, cnt, e = res
     got = np.frombuffer(data, np.uint8)
-    assert np.array_equal(got, orc.ca_run(n, inputs.ca_state(n, 42), steps))
+    assert np.array_equal(got, orc.ca_run(n, inputs.ca_state(n, 42), steps * k))
     assert cnt == world * (world + 1) // 2
     assert e == [float(sum(range(world)))] * 5

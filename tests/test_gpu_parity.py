@@ -350,6 +350,83 @@ def test_ca_ignores_bytes_past_the_slice(orc, rho, n):
     assert (bigA[D:] == 255).all() and (bigB[D:] == 255).all()     # nothing written past the slice
 
 
+def ca_steps_gpu(n, state, calls, k, strategy, world=1, fill=None):
+    """`calls` launches of tri_ca_steps(k) per rank, ranks emulated on one GPU with
+    deep halos (k packed rows from the owning rank)."""
+    maps = [tri.tri_map_init(n, 128, 1, g, world, 1) for g in range(world)]
+    full = torch.from_numpy(state).cuda()
+
+    def buf(c):
+        if fill is None:
+            return torch.empty(max(c, 16), dtype=torch.uint8, device="cuda")
+        return torch.full((c + 4096,), fill, dtype=torch.uint8, device="cuda")[:max(c, 16)]
+
+    cur = []
+    for mp in maps:
+        b = buf(mp.out_cells)
+        b[:mp.out_cells].copy_(full[mp.out_offset: mp.out_offset + mp.out_cells])
+        cur.append(b)
+    nxt = [buf(mp.out_cells) for mp in maps]
+
+    def rows(r_lo, r_hi):   # packed rows [r_lo, r_hi) copied from their owners
+        out = []
+        for h, p in enumerate(maps):
+            a, b = max(r_lo, p.row_begin), min(r_hi, p.row_end)
+            if a < b:
+                out.append(cur[h][T(a) - p.out_offset: T(b) - p.out_offset])
+        return torch.cat(out).clone() if out else None
+
+    for _ in range(calls):
+        for g, mp in enumerate(maps):
+            if not mp.out_cells:
+                continue
+            above = rows(max(mp.row_begin - k, 0), mp.row_begin) if mp.row_begin > 0 else None
+            below = rows(mp.row_end, min(mp.row_end + k, n)) if mp.row_end < n else None
+            tri.tri_ca_steps(mp, strategy, k, cur[g], nxt[g], above, below)
+        sync()
+        cur, nxt = nxt, cur
+    return np.concatenate([c[:mp.out_cells].cpu().numpy() for c, mp in zip(cur, maps)])
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (17, 7), (130, 42), (1000, 7), (2049, 42)])
+def test_ca_steps_single(orc, strategy, k, n, seed):
+    st = inputs.ca_state(n, seed)
+    assert np.array_equal(ca_steps_gpu(n, st, 2, k, strategy), orc.ca_run(n, st, 2 * k))
+
+
+@pytest.mark.parametrize("world,k", [(2, 4), (3, 3), (4, 8), (3, 1)])
+def test_ca_steps_deep_halo_ranks(orc, world, k):
+    n = 2000
+    st = inputs.ca_state(n, 42)
+    assert np.array_equal(ca_steps_gpu(n, st, 3, k, "lambda", world), orc.ca_run(n, st, 3 * k))
+
+
+@pytest.mark.parametrize("k", [1, 4])
+def test_ca_steps_ignores_garbage(orc, k):
+    n = 2049
+    st = inputs.ca_state(n, 7)
+    assert np.array_equal(ca_steps_gpu(n, st, 2, k, "lambda", 1, fill=255), orc.ca_run(n, st, 2 * k))
+
+
+def test_ca_steps_full_size_sampled(orc):
+    """BASELINE configs[3] (n = 32768) with the bench's k = 4 launch, sampled rows."""
+    n = 32768
+    st = inputs.ca_state(n, 42)
+    m = tri.tri_map_init(n, 128)
+    a = torch.from_numpy(st).cuda()
+    b = torch.empty_like(a)
+    tri.tri_ca_steps(m, "lambda", 4, a, b)
+    sync()
+    got = b.cpu().numpy()
+    ref = st
+    for _ in range(4):
+        ref = orc.ca_step(n, ref)
+    for rb, re in [(0, 40), (16380, 16390), (32700, 32768)]:
+        assert np.array_equal(got[T(rb):T(re)], ref[T(rb):T(re)])
+
+
 def test_ca_100_steps(orc):
     n = 2048
     st = inputs.ca_state(n, 7)
