@@ -434,7 +434,7 @@ __device__ __forceinline__ void run_tile(const TripArgs &a, WarpSmem &sm, uint32
 constexpr int kWarps = 2;          // 2 x 14.4 KB of tables per CTA (static smem limit 48 KB)
 
 template <int STRAT>
-__global__ void __launch_bounds__(32 * kWarps) triplet32_kernel(TripArgs a) {
+__global__ void __launch_bounds__(32 * kWarps, 8) triplet32_kernel(TripArgs a) {
     __shared__ __align__(16) WarpSmem smem[kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem &sm = smem[warp];
