@@ -391,6 +391,33 @@ def bench_ca(rank, world, pk, steps=100):
             "value": cells / (best * 1e-3), **res}
 
 
+def bench_collide1d(rank, world, pk):
+    """§8(f)3: the paper's 1-D collision test on Eq. 5 tiles, n = 200000."""
+    import torch
+    from paper_1609_01490_b200 import dist as tdist, inputs, tri
+    n = 200000
+    iv = torch.from_numpy(inputs.intervals(n, 42, 1e-5)).cuda()
+    m = tri.tri_map_init(n, 256, 1, rank, world, 1)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    res = {}
+    for st in ("bb", "lambda"):
+        def step(st=st):
+            tri.tri_collide1d(m, st, iv, cnt)
+            tdist.allreduce_count(cnt)
+        t, _ = time_steps(step, 3, 1, world)
+        res[st + "_ms"] = round(max_over_ranks(t, world) / 3, 4)
+        res[st + "_count"] = int(cnt.item())
+    res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
+    pairs = n * (n - 1) // 2
+    ops = 4.0 * pairs / world                 # FADD d, FADD s, FADD |d|-s, FMNMX per pair
+    peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
+    ach = ops / (res["lambda_ms"] * 1e-3) / 1e12
+    res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2),
+                       "unit": "TFLOP/s (fp32 ops)", "frac": round(ach / peak, 4), "ops_per_pair": 4}
+    return {"config": "1-D collision count, n=200000 intervals, r~U[0,1e-5)", "metric": "pair tests/s",
+            "value": pairs / (res["lambda_ms"] * 1e-3), **res}
+
+
 def bench_triplet(rank, world, pk):
     import torch
     from paper_1609_01490_b200 import dist as tdist, inputs, tri
@@ -527,6 +554,7 @@ def main():
         if world == 1:
             workloads["dummy"] = bench_dummy(pk)
         workloads["collide"] = bench_collide(rank, world, pk)
+        workloads["collide1d"] = bench_collide1d(rank, world, pk)
         workloads["ca"] = bench_ca(rank, world, pk)
         workloads["triplet"] = bench_triplet(rank, world, pk)
 

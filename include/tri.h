@@ -104,6 +104,12 @@ tri_status tri_map_init(tri_map_t *map, int64_t n, int32_t rho, int32_t diag,
  * (bi, bj) = (largest i with T(i) <= omega, omega - T(i)).  ERANGE: omega >= 2^40. */
 tri_status tri_lambda(uint64_t omega, uint32_t *bi, uint32_t *bj);
 
+/* Eq. 5, the map onto the strict lower triangle, with its garbled
+ * j-term corrected (reading Q2): (i, j) = (lambda(omega).i + 1, lambda(omega).j),
+ * i.e. i = floor(sqrt(1/4 + 2 omega) + 1/2), j = omega - i(i-1)/2.  Host mirror
+ * of the device function tri_collide1d uses.  ERANGE: omega >= 2^40. */
+tri_status tri_lambda_nodiag(uint64_t omega, uint32_t *i, uint32_t *j);
+
 /* GPU self-check of the map on omega in [omega0, omega0 + count):
  * counts on device (into *d_fail, u64, zeroed by the call) every omega whose
  * lambda violates Eq. 3 (T(i) <= omega < T(i+1)) or the Eq. 1 successor rule
@@ -161,6 +167,16 @@ tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_p
  * The map must be built with diag = 1 (tiles) -- the strict filter is per pair. */
 tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
                        unsigned long long *d_count, void *stream);
+
+/* 1-D collision count (reading Q10): *d_count (u64, zeroed by
+ * the call) = number of pairs j < i with |c_i - c_j| < r_i + r_j, evaluated in IEEE
+ * fp32 as d = ci - cj, s = ri + rj, |d| < s.  d_intervals: n x 2 floats (c, r),
+ * 8-byte aligned.  rho = 256.  TRI_LAMBDA launches the T(m-1) strictly-lower tiles
+ * through Eq. 5 (tri_lambda_nodiag) then the m diagonal tiles; TRI_BB the m x m
+ * grid.  Ranks split the T(m) tiles by the plain omega range (lambda) or by the
+ * map's snapped tile rows (BB). */
+tri_status tri_collide1d(const tri_map_t *map, int32_t strategy, const float *d_intervals,
+                         unsigned long long *d_count, void *stream);
 
 /* Device workspace tri_ca_step needs (bytes; may be 0). */
 size_t tri_ca_workspace_size(const tri_map_t *map);

@@ -67,6 +67,7 @@ def lib():
         L.orc_triplet_total.argtypes = [i64, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_variant_scan.argtypes = [i32, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.orc_collide1d.argtypes = [i64, vp, i64, i64, ctypes.POINTER(u64)]
         _lib = L
     return _lib
 
@@ -179,6 +180,16 @@ def collide(spheres: np.ndarray, row_begin: int = 0, row_end: int | None = None)
     row_end = n if row_end is None else row_end
     out = u64()
     _check(lib().orc_collide(n, _ptr(s), row_begin, row_end, ctypes.byref(out)))
+    return out.value
+
+
+def collide1d(intervals: np.ndarray, row_begin: int = 0, row_end: int | None = None) -> int:
+    s = np.ascontiguousarray(intervals, np.float32)
+    assert s.ndim == 2 and s.shape[1] == 2
+    n = s.shape[0]
+    row_end = n if row_end is None else row_end
+    out = u64()
+    _check(lib().orc_collide1d(n, _ptr(s), row_begin, row_end, ctypes.byref(out)))
     return out.value
 
 

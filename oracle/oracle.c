@@ -290,6 +290,24 @@ int orc_collide(int64_t n, const float *sph, int64_t row_begin, int64_t row_end,
     return ORC_OK;
 }
 
+/* 1-D collision count (reading Q10): intervals          */
+/* [c - r, c + r]; count = #{(i,j): j < i, |ci - cj| < ri + rj} with, in IEEE  */
+/* fp32, d = ci - cj, s = ri + rj, fabsf(d) < s.  2 floats (c, r) per interval.*/
+int orc_collide1d(int64_t n, const float *iv, int64_t row_begin, int64_t row_end, uint64_t *count)
+{
+    if (n < 0 || row_begin < 0 || row_end > n || row_begin > row_end) return ORC_EINVAL;
+    uint64_t total = 0;
+    #pragma omp parallel for schedule(dynamic, 64) reduction(+:total)
+    for (int64_t i = row_begin; i < row_end; ++i)
+        for (int64_t j = 0; j < i; ++j) {
+            float d = iv[2 * i] - iv[2 * j];
+            float s = iv[2 * i + 1] + iv[2 * j + 1];
+            if (fabsf(d) < s) total += 1;
+        }
+    *count = total;
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Triangular-domain cellular automaton (P:79-80 names "cellular automata     */
 /* simulation on triangular domains" citing Conway's Life; reading Q11):       */

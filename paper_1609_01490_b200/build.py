@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtri.so")
-SOURCES = ["abi.cu", "map_eval.cu", "dummy.cu", "edm.cu", "collide.cu", "ca.cu", "triplet.cu", "rb.cu"]
+SOURCES = ["abi.cu", "map_eval.cu", "dummy.cu", "edm.cu", "collide.cu", "ca.cu", "triplet.cu", "rb.cu",
+           "collide1d.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 

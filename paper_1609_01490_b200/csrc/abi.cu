@@ -100,6 +100,24 @@ tri_status tri_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ij, unsigne
     return launch_map_eval(omega0, count, d_ij, d_fail, (cudaStream_t)stream);
 }
 
+static bool bad_map(const tri_map_t *m);
+
+tri_status tri_lambda_nodiag(uint64_t omega, uint32_t *i, uint32_t *j) {
+    if (!i || !j) return TRI_EINVAL;
+    if (omega >= TRI_OMEGA_MAX) return TRI_ERANGE;
+    lambda_nodiag(omega, *i, *j);
+    return TRI_OK;
+}
+
+tri_status tri_collide1d(const tri_map_t *map, int32_t strategy, const float *d_intervals,
+                         unsigned long long *d_count, void *stream) {
+    g_launches = 0;
+    if (bad_map(map) || (strategy != TRI_LAMBDA && strategy != TRI_BB) || !d_intervals || !d_count)
+        return TRI_EINVAL;
+    if (map->rho != 256 || (((uintptr_t)d_intervals) & 7u)) return TRI_EINVAL;
+    return launch_collide1d(*map, strategy, d_intervals, d_count, (cudaStream_t)stream);
+}
+
 tri_status tri_map_eval_variant(int32_t variant, uint64_t omega0, uint64_t count, unsigned long long *d_fail,
                                 unsigned long long *d_first, void *stream) {
     g_launches = 0;

@@ -42,6 +42,18 @@ TRI_HD void lambda_map(uint64_t w, uint32_t &bi, uint32_t &bj) {
     bj = (uint32_t)(w - t);
 }
 
+// Eq. 5, the map onto the STRICT lower triangle (no diagonal).  As
+// printed its j-term gives (1, -1) at omega = 0; reading Q2 takes
+// j = omega - i(i-1)/2 with i = floor(sqrt(1/4 + 2 omega) + 1/2), which equals
+// (lambda(omega).i + 1, lambda(omega).j) -- computed that way, so it inherits
+// lambda's integer correction and exactness.
+TRI_HD void lambda_nodiag(uint64_t w, uint32_t &bi, uint32_t &bj) {
+    uint32_t i, j;
+    lambda_map(w, i, j);
+    bi = i + 1;
+    bj = j;
+}
+
 // The paper's three square-root variants of Eq. 4 (section 4.1),
 // WITHOUT the integer correction -- exact only inside their validity range.
 // Operations are explicit round-to-nearest intrinsics (no FMA contraction) so
@@ -160,6 +172,8 @@ tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk,
 tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
                                unsigned long long *d_first, cudaStream_t st);
 tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream_t st);
+tri_status launch_collide1d(const tri_map_t &m, int strategy, const float *iv, unsigned long long *count,
+                            cudaStream_t st);
 tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,
                            const uint8_t *above, const uint8_t *below, cudaStream_t st);
 tri_status launch_edm_rb(const tri_map_t &m, const float *pts, int dim, int64_t ld, float *out, cudaStream_t st);

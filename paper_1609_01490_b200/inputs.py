@@ -43,6 +43,18 @@ def spheres_quantized(n: int, seed: int = 42, bits: int = 11, r_max: float = 0.0
     return q.astype(np.float32)
 
 
+def intervals(n: int, seed: int = 42, r_max: float = 1e-5, bits: int = 0) -> np.ndarray:
+    """1-D collision input (reading Q10): centres U[0,1), radii U[0, r_max), as (c, r)
+    fp32; bits > 0 snaps both to a 2^-bits grid (exactness pin)."""
+    g = _gen(seed)
+    c = torch.rand((n, 1), generator=g, dtype=torch.float32)
+    r = torch.rand((n, 1), generator=g, dtype=torch.float32) * np.float32(r_max)
+    out = torch.cat([c, r], dim=1).contiguous().numpy()
+    if bits:
+        out = (np.floor(out.astype(np.float64) * (1 << bits)) / (1 << bits)).astype(np.float32)
+    return out
+
+
 def ca_state(n: int, seed: int = 42, p: float = 0.5) -> np.ndarray:
     D = n * (n + 1) // 2
     u = torch.rand(D, generator=_gen(seed), dtype=torch.float32)

@@ -61,6 +61,8 @@ _lib = None
 SIGNATURES = {
     "tri_map_init": ([ctypes.POINTER(TriMap), c_i64, c_i32, c_i32, c_i32, c_i32, c_i32], c_i32),
     "tri_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
+    "tri_lambda_nodiag": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
+    "tri_collide1d": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_vp, c_vp], c_i32),
     "tri_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
     "tri_map_eval_variant": ([c_i32, c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
     "tri_dummy": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, ctypes.c_size_t, c_vp], c_i32),
@@ -136,6 +138,19 @@ def tri_lambda(omega):
     bi, bj = c_u32(), c_u32()
     _ok(lib().tri_lambda(omega, ctypes.byref(bi), ctypes.byref(bj)), "tri_lambda")
     return bi.value, bj.value
+
+
+def tri_lambda_nodiag(omega):
+    i, j = c_u32(), c_u32()
+    _ok(lib().tri_lambda_nodiag(omega, ctypes.byref(i), ctypes.byref(j)), "tri_lambda_nodiag")
+    return i.value, j.value
+
+
+def tri_collide1d(m: TriMap, strategy, intervals, count, stream=None):
+    """intervals: (n, 2) float32 CUDA tensor (centre, radius); count: int64 CUDA tensor."""
+    assert intervals.dim() == 2 and intervals.shape[1] == 2 and intervals.is_contiguous()
+    _ok(lib().tri_collide1d(ctypes.byref(m), _strategy(strategy), _ptr(intervals), _ptr(count), _stream(stream)),
+        "tri_collide1d")
 
 
 def tri_map_eval(omega0, count, d_ij, d_fail, stream=None):

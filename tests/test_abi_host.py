@@ -143,3 +143,12 @@ def test_tet_map_init(L):
         assert a.omega_end == b.omega_begin
     with pytest.raises(tri.TriError):
         tri.tet_map_init(4096, 5)
+
+
+def test_host_lambda_nodiag_vs_oracle(L, orc):
+    I, J = orc.enumerate_tri(400, diag=False)
+    for w in range(len(I)):
+        assert tri.tri_lambda_nodiag(w) == (int(I[w]), int(J[w]))
+    for w in (2**39, 2**40 - 1):
+        i, j = tri.tri_lambda_nodiag(w)
+        assert i * (i - 1) // 2 <= w < i * (i + 1) // 2 and j == w - i * (i - 1) // 2

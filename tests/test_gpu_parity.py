@@ -515,3 +515,31 @@ def test_abi_rejects_bad_buffers():
     with pytest.raises(tri.TriError):
         tri.tri_dummy(tri.tri_map_init(100, 64), "lambda", tri.TRI_DUMMY_DIGEST,
                       torch.zeros(1, dtype=torch.int64, device="cuda"))
+
+
+# ============================================================== 1-D collision (Eq. 5 tiles)
+@pytest.mark.parametrize("strategy", ["lambda", "bb"])
+@pytest.mark.parametrize("n,seed,rmax", [(1, 7, 0.1), (2, 42, 0.9), (255, 7, 0.01), (256, 42, 0.01),
+                                         (1000, 7, 0.003), (5000, 42, 2e-4), (70001, 7, 1e-5)])
+def test_collide1d(orc, strategy, n, seed, rmax):
+    iv = inputs.intervals(n, seed, rmax)
+    m = tri.tri_map_init(n, 256)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_collide1d(m, strategy, torch.from_numpy(iv).cuda(), cnt)
+    sync()
+    assert cnt.item() == orc.collide1d(iv)
+
+
+def test_collide1d_ranks_and_quantized(orc):
+    n = 30000
+    iv = inputs.intervals(n, 42, 1e-4, bits=20)
+    d = torch.from_numpy(iv).cuda()
+    for strategy in ("lambda", "bb"):
+        tot = 0
+        for g in range(3):
+            m = tri.tri_map_init(n, 256, 1, g, 3, 1)
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            tri.tri_collide1d(m, strategy, d, cnt)
+            sync()
+            tot += cnt.item()
+        assert tot == orc.collide1d(iv)

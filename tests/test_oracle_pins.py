@@ -441,3 +441,41 @@ def test_dispatch_count_rb(orc, n, rho):
     gx, gy = -(-W // rho), -(-H // rho)
     assert c["blocks"] == gx * gy and c["threads"] == gx * gy * rho * rho
     assert c["discarded"] < (W + H + rho) * rho            # waste only from block rounding
+
+
+# ---------------------------------------------------------------- 1-D collision
+def test_collide1d_hand_and_sweep(orc):
+    iv = np.array([[0.0, 0.25], [0.5, 0.25], [0.25, 0.0625], [0.9, 0.01]], np.float32)
+    # (1,0) touch exactly (|d| = s, not counted); (2,0) and (2,1) overlap; (3,*) far
+    assert orc.collide1d(iv) == 2
+    assert orc.collide1d(iv[:1]) == 0
+    # independent algorithm on a 2^-20 grid (every fp32 op exact): sort by left end
+    # and sweep, counting pairs with strict overlap of the open intervals
+    iv = inputs.intervals(20000, 7, r_max=2e-4, bits=20)
+    c, r = iv[:, 0].astype(np.float64), iv[:, 1].astype(np.float64)
+    lo, hi = c - r, c + r
+    order = np.argsort(lo, kind="stable")
+    lo_s, hi_s = lo[order], hi[order]
+    cnt = 0
+    for a in range(len(order)):
+        b = np.searchsorted(lo_s, hi_s[a], side="left")          # candidates: lo_b < hi_a
+        if b > a + 1:                                            # open overlap also needs lo_a < hi_b
+            cnt += int((hi_s[a + 1:b] > lo_s[a]).sum())
+    assert cnt > 100
+    assert orc.collide1d(iv) == cnt
+    # brute force in numpy float32 (same op sequence) on random 24-bit inputs
+    iv = inputs.intervals(700, 42, r_max=5e-3)
+    d = iv[:, None, 0] - iv[None, :, 0]
+    s = iv[:, None, 1] + iv[None, :, 1]
+    m = (np.abs(d) < s) & np.tril(np.ones((700, 700), bool), -1)
+    assert orc.collide1d(iv) == int(m.sum())
+    assert orc.collide1d(iv, 0, 300) + orc.collide1d(iv, 300, 700) == int(m.sum())
+
+
+def test_lambda_nodiag_reading_q2(orc):
+    # Eq. 5 with the corrected j-term enumerates the strict lower triangle
+    I, J = orc.enumerate_tri(60, diag=False)
+    for w in range(len(I)):
+        i = math.floor(math.sqrt(0.25 + 2 * w) + 0.5)             # Eq. 5's i-term (exact here)
+        assert (i, w - i * (i - 1) // 2) == (int(I[w]), int(J[w]))
+    assert (int(I[0]), int(J[0])) == (1, 0) and (int(I[2]), int(J[2])) == (2, 1)
