@@ -164,7 +164,7 @@ tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, i
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
     if (map->rho != 32 && map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
     if (dim < 1 || dim > 4 || ld < dim) return TRI_EINVAL;
-    if (((uintptr_t)d_out & 15u) != 0) return TRI_EINVAL;
+    if (((uintptr_t)d_out & (map->rho == 256 ? 31u : 15u)) != 0) return TRI_EINVAL;   // 32-B chunks at rho 256
     if (out_bytes < map->out_cells * 4u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
     if (strategy == TRI_RB) return launch_edm_rb(*map, d_pts, dim, ld, d_out, (cudaStream_t)stream);

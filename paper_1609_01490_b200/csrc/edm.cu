@@ -4,20 +4,21 @@
 // Tile = rho x rho cells, tile coordinate from lambda(omega) (Eq. 4) or the BB
 // grid.  The packed Eq. 1 layout puts row i at T(i), so a tile's
 // row segment starts at an arbitrary 4-byte offset.  To issue only aligned
-// 16-byte streaming stores, every aligned 4-float CHUNK of the output slice is
-// owned by the tile that holds the chunk's first cell; the owner computes all
-// four cells even when they run past the tile edge (EDM is pointwise, so the
+// vector streaming stores, every aligned CW-float CHUNK of the output slice
+// (CW = 4: 16 B; CW = 8 at rho = 256: 32 B, the sm_100 256-bit store) is owned
+// by the tile that holds the chunk's first cell; the owner computes all CW
+// cells even when they run past the tile edge (EDM is pointwise, so the
 // neighbour cells are computable anywhere).
 //
 // Interior tiles (bj + 1 < bi: every chunk stays inside its row) take the
-// fast path: one warp walks ROWS rows of the tile; lane k owns chunk slots
-// k, k+32, ... (CPL = rho/128 chunks per lane per row, interleaved so each
-// store instruction is one 512-byte contiguous run).  The row's chunk phase
-// delta = (-T(i)) mod 4 is warp-uniform, so every lane takes its 4 columns
-// from a 7-column register window with a uniform switch; the row offset is
-// advanced incrementally (T(i+1) = T(i) + i + 1) and the row point is
-// broadcast by shuffle.  Tiles touching the diagonal (bj >= bi - 1) take a
-// checked path that walks Eq. 1 across row ends and the slice end.
+// fast path: one warp walks ROWS rows of the tile, lane k owning chunk k
+// (rho = 32 CW, so each warp store is one contiguous 512 B / 1 KB run).  The
+// row's chunk phase delta = (-T(i)) mod CW is warp-uniform, so every lane takes
+// its CW columns from a (2 CW - 1)-column register window through a uniform
+// branch; the row offset is advanced incrementally (T(i+1) = T(i) + i + 1) and
+// the row point is broadcast by shuffle.  Tiles touching the diagonal
+// (bj >= bi - 1) take a checked path that walks Eq. 1 across row ends and the
+// slice end.
 #include "tri_common.cuh"
 
 namespace {
@@ -34,8 +35,14 @@ struct EdmArgs {
 constexpr int kEdmThreads = 256;
 constexpr int kWarps = kEdmThreads / 32;
 
-template <int DIM>
-__device__ __forceinline__ float dist_w(const float (&p)[DIM], const float (&w)[DIM][7], int t) {
+// Chunk width (floats) per tile edge: rho = 256 uses 32-byte chunks and the
+// sm_100 256-bit store (STG.E.ENL2.256, 1 KB per warp store), rho = 128 16-byte
+// chunks (512 B); a launch uses one chunk width for all its tiles, so chunk
+// ownership is consistent across tiles.
+template <int RHO> struct ChunkW { static constexpr int CW = RHO == 256 ? 8 : 4; };
+
+template <int DIM, int WN>
+__device__ __forceinline__ float dist_w(const float (&p)[DIM], const float (&w)[DIM][WN], int t) {
     const float dx = p[0] - w[0][t];
     float d2 = dx * dx;
 #pragma unroll
@@ -57,30 +64,56 @@ __device__ __forceinline__ float dist_gmem(const EdmArgs &a, int64_t i, int64_t 
     return sqrt_approx(d2);
 }
 
-template <int DIM, int D>
-__device__ __forceinline__ void chunk4(const float (&p)[DIM], const float (&w)[DIM][7], float *dst) {
-    st_cs_v4(dst, dist_w<DIM>(p, w, D), dist_w<DIM>(p, w, D + 1), dist_w<DIM>(p, w, D + 2),
-             dist_w<DIM>(p, w, D + 3));
+__device__ __forceinline__ void st_cs_v8(float *p, const float (&v)[8]) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
+template <int CW>
+__device__ __forceinline__ void store_chunk(float *dst, const float (&v)[CW]) {
+    if constexpr (CW == 8) st_cs_v8(dst, v);
+    else st_cs_v4(dst, v[0], v[1], v[2], v[3]);
+}
+
+// one lane's chunk at window offset D (the row's phase delta)
+template <int DIM, int CW, int D>
+__device__ __forceinline__ void chunk_at(const float (&p)[DIM], const float (&w)[DIM][2 * CW - 1], float *dst) {
+    float v[CW];
+#pragma unroll
+    for (int e = 0; e < CW; ++e) v[e] = dist_w<DIM, 2 * CW - 1>(p, w, D + e);
+    store_chunk<CW>(dst, v);
+}
+
+// warp-uniform dispatch on delta in [0, CW)
+template <int DIM, int CW, int D = 0>
+__device__ __forceinline__ void chunk_phase(int delta, const float (&p)[DIM], const float (&w)[DIM][2 * CW - 1],
+                                            float *dst) {
+    if (delta == D) {
+        chunk_at<DIM, CW, D>(p, w, dst);
+    } else if constexpr (D + 1 < CW) {
+        chunk_phase<DIM, CW, D + 1>(delta, p, w, dst);
+    }
 }
 
 // Interior tile: rows [r0, r0+RHO) x cols [c0, c0+RHO), c0 + RHO < r0.
+// One warp per row segment: lane k owns chunk k (RHO = 32 CW).
 template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, int64_t c0) {
-    constexpr int CPL = RHO / 128;                // chunk slots per lane per row
+    constexpr int CW = ChunkW<RHO>::CW, WN = 2 * CW - 1;
+    static_assert(RHO == 32 * CW, "one chunk per lane per row");
     constexpr int ROWS = RHO / kWarps;            // rows per warp (<= 32)
     static_assert(ROWS <= 32, "row points are broadcast from one lane each");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t rbase = r0 + (int64_t)warp * ROWS;
     if (rbase >= a.n) return;
-    float w[CPL][DIM][7];
+    float w[DIM][WN];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c)
+    for (int t = 0; t < WN; ++t) {
+        const int64_t col = c0 + CW * lane + t;               // < r0: always a valid point
 #pragma unroll
-        for (int t = 0; t < 7; ++t) {
-            const int64_t col = c0 + 128 * c + 4 * lane + t;    // < r0 <= n - 1 + ... always in range
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) w[c][d][t] = __ldg(a.pts + col * a.ld + d);
-        }
+        for (int d = 0; d < DIM; ++d) w[d][t] = __ldg(a.pts + col * a.ld + d);
+    }
     float pr[DIM];
     {
         const int64_t rr = rbase + (lane < ROWS ? lane : 0);
@@ -90,32 +123,14 @@ __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, 
     }
     const int nrows = (int)((a.n - rbase) < ROWS ? (a.n - rbase) : ROWS);
     uint64_t s = tri::T2((uint64_t)rbase) + (uint64_t)c0 - a.out_offset;   // local start of row rbase
-    float *base = a.out + 4 * lane;
+    float *base = a.out + CW * lane;
 #pragma unroll 1
     for (int rr = 0; rr < nrows; ++rr) {
         float p[DIM];
 #pragma unroll
         for (int d = 0; d < DIM; ++d) p[d] = __shfl_sync(0xffffffffu, pr[d], rr);
-        const int delta = (int)((0u - (uint32_t)s) & 3u);
-        float *dst = base + (s + (uint64_t)delta);
-        switch (delta) {
-            case 0:
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) chunk4<DIM, 0>(p, w[c], dst + 128 * c);
-                break;
-            case 1:
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) chunk4<DIM, 1>(p, w[c], dst + 128 * c);
-                break;
-            case 2:
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) chunk4<DIM, 2>(p, w[c], dst + 128 * c);
-                break;
-            default:
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) chunk4<DIM, 3>(p, w[c], dst + 128 * c);
-                break;
-        }
+        const int delta = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1));
+        chunk_phase<DIM, CW>(delta, p, w, base + (s + (uint64_t)delta));
         s += (uint64_t)(rbase + rr + 1);               // T(i+1) = T(i) + i + 1
     }
 }
@@ -124,7 +139,8 @@ __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, 
 // chunk slot of every row, cells walked along Eq. 1, all bounds checked.
 template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, int64_t c0) {
-    constexpr int L = RHO / 4;                        // chunk slots per row segment
+    constexpr int CW = ChunkW<RHO>::CW;
+    constexpr int L = RHO / CW;                       // chunk slots per row segment
     const int t = threadIdx.x;
 #pragma unroll 1
     for (int q = t; q < RHO * L; q += kEdmThreads) {
@@ -134,23 +150,23 @@ __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, i
         const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.out_offset;
         const int64_t seg = i - c0 + 1;
         const int64_t len = seg < RHO ? seg : RHO;
-        const int off = (int)((0u - (uint32_t)s) & 3u) + 4 * k;
+        const int off = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1)) + CW * k;
         if (off >= len) continue;                      // chunk owned by the next segment
         const uint64_t c = s + (uint64_t)off;
-        float v[4];
+        float v[CW];
         int64_t ii = i, jj = c0 + off;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < CW; ++e) {
             while (jj > ii) { jj -= ii + 1; ++ii; }
             v[e] = (c + e < a.out_cells && ii < a.n) ? dist_gmem<DIM>(a, ii, jj) : 0.f;
             ++jj;
         }
         float *dst = a.out + c;
-        if (c + 4 <= a.out_cells) {
-            st_cs_v4(dst, v[0], v[1], v[2], v[3]);
+        if (c + CW <= a.out_cells) {
+            store_chunk<CW>(dst, v);
         } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
+            for (int e = 0; e < CW; ++e)
                 if (c + e < a.out_cells) dst[e] = v[e];
         }
     }
@@ -257,11 +273,11 @@ extern "C" tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const
     reset_launches();
     if (!map || !h_pts || !d_pts_ws || !h_out || !d_ws) return TRI_EINVAL;
     if (!map->diag || map->rho < 1) return TRI_EINVAL;
-    if (out_bytes < map->out_cells * 4u || (((uintptr_t)d_ws) & 15u)) return TRI_EINVAL;
-    uint64_t cap = (ws_bytes / 2 / 4) & ~3ull;          // floats per buffer, 16-byte multiple
-    if (band_cells && band_cells < cap) cap = band_cells & ~3ull;
+    if (out_bytes < map->out_cells * 4u || (((uintptr_t)d_ws) & 31u)) return TRI_EINVAL;
+    uint64_t cap = (ws_bytes / 2 / 4) & ~7ull;          // floats per buffer, 32-byte multiple
+    if (band_cells && band_cells < cap) cap = band_cells & ~7ull;
     const int64_t rho = map->rho;
-    float *buf[2] = {(float *)d_ws, (float *)d_ws + ((ws_bytes / 2 / 4) & ~3ull)};
+    float *buf[2] = {(float *)d_ws, (float *)d_ws + ((ws_bytes / 2 / 4) & ~7ull)};
     cudaStream_t sc = nullptr, sx = nullptr;
     cudaEvent_t done_k[2] = {nullptr, nullptr}, done_c[2] = {nullptr, nullptr};
     tri_status rc = TRI_OK;
