@@ -427,6 +427,50 @@ def test_ca_steps_full_size_sampled(orc):
         assert np.array_equal(got[T(rb):T(re)], ref[T(rb):T(re)])
 
 
+@pytest.mark.slow
+def test_large_n_64bit_offsets(orc):
+    """n = 200000: 2.0e10 packed cells (> 2^32) -- EDM (80 GB) and one CA generation
+    (2 x 20 GB) through the 64-bit index paths, sampled rows vs the oracle."""
+    n = 200000
+    D = T(n)
+    assert D > 2**34
+    pts = inputs.points(n, 3, 7)
+    m = tri.tri_map_init(n, 128)
+    out = torch.empty(D, dtype=torch.float32, device="cuda")
+    tri.tri_edm(m, "lambda", torch.from_numpy(pts).cuda(), out)
+    sync()
+    for rb, re in [(0, 8), (92681, 92684), (199997, 200000)]:        # T(92681) crosses 2^32
+        edm_close(out[T(rb):T(re)].cpu().numpy(), orc.edm(pts, rb, re))
+    del out
+    torch.cuda.empty_cache()
+    # CA just past 2^32 cells (n = 92800: 4.31e9 bytes); Bernoulli(0.5) bits from a
+    # seeded numpy generator (the torch generator would need 17 GB of host floats)
+    n = 92800
+    D = T(n)
+    assert D > 2**32
+    st = np.random.default_rng(7).integers(0, 2, size=D, dtype=np.uint8)
+    m = tri.tri_map_init(n, 128)
+    a = torch.from_numpy(st).cuda()
+    b = torch.empty_like(a)
+    tri.tri_ca_step(m, "lambda", a, b)
+    sync()
+    for rb, re in [(92680, 92683), (92797, 92800)]:                  # T(92681) crosses 2^32
+        assert np.array_equal(b[T(rb):T(re)].cpu().numpy(), orc.ca_step_rows(n, st, rb, re))
+    tri.tri_ca_steps(m, "lambda", 3, a, b)
+    sync()
+    for rb, re in [(92680, 92683), (92790, 92800)]:
+        lo, hi = rb - 3, min(re + 3, n)          # light cone: 3 generations of rows [lo, hi)
+        work = np.zeros(D, np.uint8)            # are exact on [rb, re)
+        work[T(lo):T(hi)] = st[T(lo):T(hi)]
+        for _ in range(3):
+            nxt = np.zeros(D, np.uint8)
+            nxt[T(lo):T(hi)] = orc.ca_step_rows(n, work, lo, hi)
+            work = nxt
+        assert np.array_equal(b[T(rb):T(re)].cpu().numpy(), work[T(rb):T(re)])
+    del a, b
+    torch.cuda.empty_cache()
+
+
 def test_ca_100_steps(orc):
     n = 2048
     st = inputs.ca_state(n, 7)
