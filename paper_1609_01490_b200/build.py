@@ -40,7 +40,9 @@ def _compile(src: str, verbose: bool) -> str:
     cmd = [_nvcc(), *ARCH, *FLAGS, "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:
-        f.write(r.stdout + r.stderr)
+        # drop ptxas' wall-clock lines so the tracked logs only change with the code
+        f.write("".join(l for l in (r.stdout + r.stderr).splitlines(True)
+                        if "Compile time" not in l))
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed on {src}")
