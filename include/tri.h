@@ -24,8 +24,13 @@
  *                          coordinate = lambda(omega) (Eq. 4);
  *      TRI_BB              m x m grid, tiles above the diagonal exit on a
  *                          block test, diagonal tiles filter per thread;
- *      TRI_LAMBDA_PERSIST  a grid of (SMs x resident CTAs) CTAs walking omega
- *                          with a stride, lambda per tile (the B200 form).
+ *      TRI_LAMBDA_PERSIST  a grid of (SMs x resident CTAs) CTAs, each walking
+ *                          a contiguous omega chunk: lambda once at the chunk
+ *                          start, then the Eq. 1 successor rule;
+ *      TRI_LAMBDA_CLC      (tri_edm only) the TRI_LAMBDA grid run by
+ *                          persistent CTAs that take further tiles by
+ *                          cancelling not-yet-launched CTAs (sm_100 cluster
+ *                          launch control), lambda per tile.
  */
 #ifndef TRI_H_
 #define TRI_H_
@@ -45,7 +50,7 @@ typedef enum {
     TRI_ENOTSUP = -4  /* valid request this build does not implement                   */
 } tri_status;
 
-enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2 };
+enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2, TRI_LAMBDA_CLC = 7 };
 /* The paper's square-root variants of Eq. 4 (section 4.1), used WITHOUT
  * the integer correction: lambda_X = IEEE sqrtf, lambda_N = 0x5f3759df seed + 3
  * Newton steps + eps, lambda_R = x * rsqrtf(x) + eps, eps = 1e-4.  Exact only

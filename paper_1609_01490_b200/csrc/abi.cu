@@ -160,7 +160,9 @@ tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode, void 
 tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, int32_t dim, int64_t ld,
                    float *d_out, size_t out_bytes, void *stream) {
     g_launches = 0;
-    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_RB) || !d_pts || !d_out) return TRI_EINVAL;
+    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_RB && strategy != TRI_LAMBDA_CLC) || !d_pts ||
+        !d_out)
+        return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
     if (map->rho != 32 && map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
     if (dim < 1 || dim > 4 || ld < dim) return TRI_EINVAL;

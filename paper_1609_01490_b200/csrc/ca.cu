@@ -652,10 +652,8 @@ __global__ void __launch_bounds__(Cfg<RHO>::NT) ca_bits_kernel(CaArgs a) {
     } else {
         uint32_t parity = 0;
 #pragma unroll 1
-        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
-            uint32_t bi, bj;
-            tri::lambda_map(w, bi, bj);
-            tile<RHO>(a, bi, bj, sm, parity);
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
+            tile<RHO>(a, t.bi, t.bj, sm, parity);
             parity ^= 1u;
             // generic-proxy reads of the staging buffer before the next tile's TMA writes
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -901,10 +899,8 @@ __global__ void __launch_bounds__(NT) ca_multi_kernel(CaArgs a) {
     } else {
         uint32_t parity = 0;
 #pragma unroll 1
-        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
-            uint32_t bi, bj;
-            tri::lambda_map(w, bi, bj);
-            tile(a, bi, bj, sm, parity);
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
+            tile(a, t.bi, t.bj, sm, parity);
             parity ^= 1u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
@@ -956,11 +952,7 @@ __global__ void __launch_bounds__(kCaThreads) ca_kernel(CaArgs a) {
         ca_tile<RHO>(a, bi, bj);
     } else {
 #pragma unroll 1
-        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
-            uint32_t bi, bj;
-            tri::lambda_map(w, bi, bj);
-            ca_tile<RHO>(a, bi, bj);
-        }
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) ca_tile<RHO>(a, t.bi, t.bj);
     }
 }
 

@@ -172,11 +172,8 @@ __global__ void __launch_bounds__(RHO / K) collide_kernel(CollideArgs a) {
         cnt = collide_tile<RHO>(a, bi, bj, smem);
     } else {
 #pragma unroll 1
-        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
-            uint32_t bi, bj;
-            tri::lambda_map(w, bi, bj);
-            cnt += collide_tile<RHO>(a, bi, bj, smem);
-        }
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next())
+            cnt += collide_tile<RHO>(a, t.bi, t.bj, smem);
     }
     flush_count<RHO / K>(cnt, a.count);
 }

@@ -89,12 +89,8 @@ __global__ void __launch_bounds__(RHO * RHO) dummy_kernel(DummyArgs a) {
         tri::lambda_variant(w, STRAT - TRI_LAMBDA_X + TRI_SQRT_X, bi, bj);
         if (bj > bi || (int64_t)bi * RHO >= a.n) return;
         dummy_body<RHO, MODE>(a, bi, bj, &acc);
-    } else {  // persistent
-        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
-            uint32_t bi, bj;
-            tri::lambda_map(w, bi, bj);
-            dummy_body<RHO, MODE>(a, bi, bj, &acc);
-        }
+    } else {  // persistent lambda-walk
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) dummy_body<RHO, MODE>(a, t.bi, t.bj, &acc);
     }
     if (MODE == TRI_DUMMY_DIGEST) {
         const unsigned long long s = block_sum<RHO * RHO>(acc);
@@ -104,8 +100,8 @@ __global__ void __launch_bounds__(RHO * RHO) dummy_kernel(DummyArgs a) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
             unsigned long long tiles = 1;
             if (STRAT == TRI_LAMBDA_PERSIST) {
-                tiles = 0;
-                for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) ++tiles;
+                const tri::TileWalk t(a.omega_begin, a.omega_end);
+                tiles = t.end - t.w;
             }
             atomicAdd(&cnt[0], tiles);
             atomicAdd(&cnt[2], tiles * RHO * RHO);

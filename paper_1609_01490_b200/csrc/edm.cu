@@ -194,13 +194,27 @@ __global__ void __launch_bounds__(kEdmThreads) edm_kernel(EdmArgs a) {
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
         edm_tile<RHO, DIM>(a, bi, bj);
+    } else if (STRAT == TRI_LAMBDA_CLC) {
+        __shared__ tri::ClcSched clc;
+        if (threadIdx.x == 0) clc.init();
+        __syncthreads();
+        uint32_t bx = blockIdx.x, by = blockIdx.y, phase = 0;
+#pragma unroll 1
+        while (true) {
+            if (threadIdx.x == 0) clc.request();              // overlaps the tile below
+            const uint64_t w = a.omega_begin + (uint64_t)by * gridDim.x + bx;
+            if (w < a.omega_end) {
+                uint32_t bi, bj;
+                tri::lambda_map(w, bi, bj);
+                edm_tile<RHO, DIM>(a, bi, bj);
+            }
+            const bool more = clc.receive(phase, bx, by);
+            __syncthreads();                                  // handle read by all before the next request
+            if (!more) break;
+        }
     } else {
 #pragma unroll 1
-        for (uint64_t w = a.omega_begin + blockIdx.x; w < a.omega_end; w += gridDim.x) {
-            uint32_t bi, bj;
-            tri::lambda_map(w, bi, bj);
-            edm_tile<RHO, DIM>(a, bi, bj);
-        }
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) edm_tile<RHO, DIM>(a, t.bi, t.bj);
     }
 }
 
@@ -217,6 +231,10 @@ tri_status launch_rd(const tri_map_t &m, int strategy, EdmArgs a, cudaStream_t s
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
         edm_kernel<RHO, DIM, TRI_LAMBDA><<<tri::tile_grid(nb), kEdmThreads, 0, st>>>(a);
+    } else if (strategy == TRI_LAMBDA_CLC) {
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (!nb) return TRI_OK;
+        edm_kernel<RHO, DIM, TRI_LAMBDA_CLC><<<tri::tile_grid(nb), kEdmThreads, 0, st>>>(a);
     } else {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;

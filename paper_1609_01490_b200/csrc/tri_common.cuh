@@ -126,6 +126,88 @@ TRI_HD void tet_map(uint64_t w, uint32_t &i, uint32_t &j, uint32_t &k) {
     lambda_map(w - t, i, j);
 }
 
+// Persistent lambda-walk: CTA c of the grid owns the contiguous
+// omega chunk [begin + c*q + min(c, r), ...) of the balanced split of
+// [begin, end) (q = nb / grid, r = nb % grid), evaluates lambda ONCE at the
+// chunk start and then steps with the Eq. 1 successor rule (j + 1, wrapping to
+// (i + 1, 0) past the diagonal).  Consecutive tiles -- and the output rows they
+// share -- stay in one CTA, so the straddling 32-B sectors are completed while
+// still in L2 (a grid-stride loop scatters them across CTAs that drift apart).
+struct TileWalk {
+    uint64_t w, end;
+    uint32_t bi, bj;
+    __device__ __forceinline__ TileWalk(uint64_t begin, uint64_t stop) {
+        const uint64_t nb = stop - begin, g = gridDim.x, c = blockIdx.x;
+        const uint64_t q = nb / g, r = nb % g;
+        w = begin + c * q + (c < r ? c : r);
+        end = w + q + (c < r ? 1 : 0);
+        bi = bj = 0;
+        if (w < end) lambda_map(w, bi, bj);
+    }
+    __device__ __forceinline__ bool more() const { return w < end; }
+    __device__ __forceinline__ void next() {
+        ++w;
+        if (++bj > bi) { ++bi; bj = 0; }
+    }
+};
+
+// Persistent CTAs with hardware work-stealing (sm_100 cluster launch control).
+// The grid is the full lambda grid; a running CTA, after finishing a tile,
+// cancels the next not-yet-launched CTA (clusterlaunchcontrol.try_cancel) and
+// processes that CTA's tile instead, so tiles keep the hardware's omega-order
+// dispatch (neighbouring tiles in flight together) while the CTA prologue,
+// shared-memory setup and L1 contents persist.  One 16-B response + one
+// mbarrier per CTA, in shared memory.
+struct ClcSched {
+    uint4 handle;
+    unsigned long long mbar;
+    __device__ __forceinline__ uint32_t hs() const { return (uint32_t)__cvta_generic_to_shared(&handle); }
+    __device__ __forceinline__ uint32_t mb() const { return (uint32_t)__cvta_generic_to_shared(&mbar); }
+    // one thread, before the first request; a __syncthreads() must follow
+    __device__ __forceinline__ void init() {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb()));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // one thread: ask for the next CTA (asynchronous; the response lands in handle)
+    __device__ __forceinline__ void request() {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16;" ::"r"(mb()) : "memory");
+        asm volatile(
+            "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+                hs()),
+            "r"(mb())
+            : "memory");
+    }
+    // every thread: wait for the response; returns false when no CTA was left.
+    // The caller must __syncthreads() before the next request() reuses handle.
+    __device__ __forceinline__ bool receive(uint32_t &phase, uint32_t &bx, uint32_t &by) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p;\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                "selp.b32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(mb()), "r"(phase)
+                : "memory");
+        phase ^= 1u;
+        uint32_t ok, x, y, z;
+        asm volatile(
+            "{ .reg .b128 h; .reg .pred p;\n"
+            "ld.shared.b128 h, [%4];\n"
+            "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, h;\n"
+            "selp.b32 %0, 1, 0, p;\n"
+            "clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%1, %2, %3, _}, h; }"
+            : "=r"(ok), "=r"(x), "=r"(y), "=r"(z)
+            : "r"(hs())
+            : "memory");
+        // order this generic-proxy read before the next request's async-proxy write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bx = x;
+        by = y;
+        return ok != 0;
+    }
+};
+
 }  // namespace tri
 
 // ------------------------------------------------------------------ device stores

@@ -16,11 +16,13 @@ LIB_PATH = os.path.join(HERE, "libtri.so")
 
 TRI_OK, TRI_EINVAL, TRI_ERANGE, TRI_ECUDA, TRI_ENOTSUP = 0, -1, -2, -3, -4
 TRI_LAMBDA, TRI_BB, TRI_LAMBDA_PERSIST = 0, 1, 2
+TRI_LAMBDA_CLC = 7                                           # persistent CTAs, cluster launch control
 TRI_DUMMY_FIXED, TRI_DUMMY_PACKED, TRI_DUMMY_DIGEST, TRI_DUMMY_COUNT = 0, 1, 2, 3
 TRI_LAMBDA_X, TRI_LAMBDA_N, TRI_LAMBDA_R = 3, 4, 5          # tri_dummy only (section 4.1 variants)
 TRI_SQRT_X, TRI_SQRT_N, TRI_SQRT_R = 1, 2, 3
 STRATEGIES = {"lambda": TRI_LAMBDA, "bb": TRI_BB, "persist": TRI_LAMBDA_PERSIST,
-              "lambda_x": TRI_LAMBDA_X, "lambda_n": TRI_LAMBDA_N, "lambda_r": TRI_LAMBDA_R, "rb": 6}
+              "lambda_x": TRI_LAMBDA_X, "lambda_n": TRI_LAMBDA_N, "lambda_r": TRI_LAMBDA_R, "rb": 6,
+              "clc": TRI_LAMBDA_CLC}
 TRI_RB = 6                                                   # tri_dummy / tri_edm, single rank
 
 c_u64, c_i64, c_i32, c_u32, c_vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p

@@ -180,7 +180,7 @@ def edm_close(got, ref):
     assert not bad.any(), (int(bad.sum()), float(err.max()))
 
 
-@pytest.mark.parametrize("strategy", STRATS + ["rb"])
+@pytest.mark.parametrize("strategy", STRATS + ["rb", "clc"])
 @pytest.mark.parametrize("rho", [32, 64, 128, 256])
 @pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (3, 7), (5, 42), (64, 7), (257, 42), (1000, 7), (4097, 42)])
 def test_edm_small(orc, strategy, rho, n, seed):
@@ -222,14 +222,14 @@ def test_edm_ranks_concatenate(orc, world, rho):
     edm_close(np.concatenate(parts), orc.edm(pts))
 
 
-@pytest.mark.parametrize("rho", [128, 256])
-def test_edm_full_size_sampled(orc, rho):
-    """BASELINE configs[1]: n = 65536, 3-D, the bench's launch (persistent lambda)."""
+@pytest.mark.parametrize("strategy,rho", [("lambda", 128), ("lambda", 256), ("persist", 128), ("clc", 128)])
+def test_edm_full_size_sampled(orc, strategy, rho):
+    """BASELINE configs[1]: n = 65536, 3-D; ("lambda", 128) is the bench's launch."""
     n = 65536
     pts = inputs.points(n, 3, 42)
     m = tri.tri_map_init(n, rho)
     out = torch.full((m.out_cells,), float("nan"), dtype=torch.float32, device="cuda")
-    tri.tri_edm(m, "persist", torch.from_numpy(pts).cuda(), out)
+    tri.tri_edm(m, strategy, torch.from_numpy(pts).cuda(), out)
     sync()
     assert not torch.isnan(out).any().item()           # every cell written
     for rb, re in [(0, 64), (20000, 20030), (40961, 40970), (65500, 65536)]:
