@@ -708,18 +708,21 @@ constexpr int RHO = 128;
 constexpr int KMAX = 8;
 constexpr int NINMAX = RHO + 2 * KMAX;   // input rows
 constexpr int NW = 5;                    // bitmap words per row: bit x <-> column c0 - k + x (rho + 2k <= 160)
-constexpr int NT = 32 * NW;              // 160 threads: phase B = NW words x 32 bands
-constexpr int RAWB = 32 * (NW + 1);      // staged bytes per row (>= 15 + rho + 2k)
+constexpr int RB = 4;                     // phase B: rows per band (register-resident)
+constexpr int BPW = 32 / NW;             // bands per warp (6: lanes 0..29, lanes 30, 31 idle in B)
+constexpr int NBAND = NINMAX / RB;       // 36 bands x 4 rows = the 144-row region
+constexpr int NT = 32 * ((NBAND + BPW - 1) / BPW);   // 192 threads
+static_assert(NBAND * RB == NINMAX, "bands tile the region");
+constexpr int RAWB = 32 * (NW + 1);      // loaded bytes per row (>= 15 + rho + 2k)
 constexpr int NCH = RAWB / 16;
-constexpr int STRIDE = RAWB + 16;        // 16 (mod 128): conflict-free LDS.128 across rows
-constexpr int SLOTS = RHO / 16 + 1;      // 16-byte chunks a row segment can touch
 
 struct Smem {
-    uint32_t A[NINMAX][NW], B[NINMAX][NW], M[NINMAX][NW];   // ping-pong bitmaps, triangle masks
-    alignas(16) uint8_t raw[NINMAX][STRIDE];
+    uint32_t A[NINMAX][NW];                   // packed region (phase A) / final state (phase C)
+    uint32_t top[2][NBAND][NW], bot[2][NBAND][NW];   // band edge rows, double-buffered by generation
     uint64_t seg[RHO];
-    alignas(8) unsigned long long bar;
 };
+
+template <bool B> struct MaskTag { static constexpr bool value = B; };
 
 // bits of columns [cb, cb + 32) that lie inside row r of the triangle
 __device__ __forceinline__ uint32_t tri_mask(int64_t r, int64_t n, int64_t cb) {
@@ -731,140 +734,180 @@ __device__ __forceinline__ uint32_t tri_mask(int64_t r, int64_t n, int64_t cb) {
     return up & ~((1u << lo) - 1u);
 }
 
-__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm, uint32_t parity) {
+__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
     const int t = threadIdx.x;
     const int K = (int)a.k;
     const int NIN = RHO + 2 * K;
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
     const int64_t cs = c0 - K;                        // column of bitmap bit 0
-    // ---- A: stage + pack rows r0-K .. r0+RHO+K-1 (thread t = input row t)
-    if (t < NINMAX) {
-        if (t < NIN) {
-            const int64_t r = r0 - K + t;
-            if (t >= K && t < K + RHO) sm.seg[t - K] = tri::T2((uint64_t)r) + (uint64_t)c0 - a.base;
-            uint8_t *dst = sm.raw[t];
-            const uint8_t *p = row_ptr(a, r);
-            uint32_t e = 0;
-            if (!p) {
+    // ---- A: load + pack rows r0-K .. r0+RHO+K-1 (thread t = input row t): the
+    // row's 16-byte-aligned window straight into registers (read-only path),
+    // bytes outside the row masked before packing.  (Per-row cp.async.bulk
+    // copies serialise on the uniform datapath -- one ELECT/R2UR round per lane
+    // -- which made staging 40 % of the tile time.)
+    if (t < NIN) {
+        const int64_t r = r0 - K + t;
+        if (t >= K && t < K + RHO) sm.seg[t - K] = tri::T2((uint64_t)r) + (uint64_t)c0 - a.base;
+        const uint8_t *p = row_ptr(a, r);
+        if (!p) {
 #pragma unroll
-                for (int h = 0; h < NCH; ++h) *reinterpret_cast<uint4 *>(dst + 16 * h) = make_uint4(0, 0, 0, 0);
-                bits::mbar_arrive(&sm.bar);
-            } else {
-                const uintptr_t Ad = (uintptr_t)(p + cs);
-                e = (uint32_t)(Ad & 15u);
-                const int64_t col0 = cs - (int64_t)e;
-                const uint4 *q = (const uint4 *)(Ad & ~(uintptr_t)15);
-                if (col0 >= 0 && col0 + RAWB - 1 <= r) {
-                    bits::mbar_arrive_tx(&sm.bar, RAWB);
-                    bits::bulk_g2s(dst, q, RAWB, &sm.bar);
-                } else {
-#pragma unroll
-                    for (int h = 0; h < NCH; ++h) {
-                        const int64_t cb = col0 + 16 * h;
-                        const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
-                        uint4 c = make_uint4(0, 0, 0, 0);
-                        if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
-                            c = __ldg(q + h);
-                            bits::mask_chunk(c, lo_c, hi_c);
-                        }
-                        *reinterpret_cast<uint4 *>(dst + 16 * h) = c;
-                    }
-                    bits::mbar_arrive(&sm.bar);
-                }
-            }
-            bits::mbar_wait(&sm.bar, parity);
-            uint32_t prev = 0;
-#pragma unroll
-            for (int v = 0; v <= NW; ++v) {
-                const uint32_t lo = bits::pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v));
-                const uint32_t hi = bits::pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v + 16));
-                const uint32_t P = lo | (hi << 16);
-                if (v > 0) {
-                    const uint32_t mk = tri_mask(r, a.n, cs + 32 * (v - 1));
-                    sm.M[t][v - 1] = mk;
-                    sm.A[t][v - 1] = __funnelshift_r(prev, P, e) & mk;
-                }
-                prev = P;
-            }
+            for (int v = 0; v < NW; ++v) sm.A[t][v] = 0u;
         } else {
-            // rows the mbarrier counts but this K does not use
-            bits::mbar_arrive(&sm.bar);
+            const uintptr_t Ad = (uintptr_t)(p + cs);
+            const uint32_t e = (uint32_t)(Ad & 15u);
+            const int64_t col0 = cs - (int64_t)e;
+            const uint4 *q = (const uint4 *)(Ad & ~(uintptr_t)15);
+            if (col0 >= 0 && col0 + RAWB - 1 <= r) {
+                // whole window inside the row (hence inside the triangle): no masks
+                uint4 c[NCH];
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) c[h] = __ldg(q + h);
+                uint32_t prev = bits::pack16(c[0]) | (bits::pack16(c[1]) << 16);
+#pragma unroll
+                for (int v = 1; v <= NW; ++v) {
+                    const uint32_t P = bits::pack16(c[2 * v]) | (bits::pack16(c[2 * v + 1]) << 16);
+                    sm.A[t][v - 1] = __funnelshift_r(prev, P, e);
+                    prev = P;
+                }
+            } else {
+                uint4 c[NCH];
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) {
+                    const int64_t cb = col0 + 16 * h;
+                    const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
+                    c[h] = make_uint4(0, 0, 0, 0);
+                    if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
+                        c[h] = __ldg(q + h);
+                        bits::mask_chunk(c[h], lo_c, hi_c);
+                    }
+                }
+                uint32_t prev = 0;
+#pragma unroll
+                for (int v = 0; v <= NW; ++v) {
+                    const uint32_t P = bits::pack16(c[2 * v]) | (bits::pack16(c[2 * v + 1]) << 16);
+                    if (v > 0)
+                        sm.A[t][v - 1] = __funnelshift_r(prev, P, e) & tri_mask(r, a.n, cs + 32 * (v - 1));
+                    prev = P;
+                }
+            }
         }
     }
     __syncthreads();
-    // ---- B: K generations, ping-pong A -> B -> A ...
-    const int w = t % NW, band = t / NW;
-#pragma unroll 1
-    for (int g = 1; g <= K; ++g) {
-        uint32_t (*src)[NW] = (g & 1) ? sm.A : sm.B;
-        uint32_t (*dst)[NW] = (g & 1) ? sm.B : sm.A;
-        const int y_lo = g, y_hi = NIN - g;                    // rows computed this generation
-        const int rows = (y_hi - y_lo + 31) / 32;
-        const int ya = y_lo + band * rows;
-        int yb = ya + rows;
-        if (yb > y_hi) yb = y_hi;
-        auto terms = [&](int y, uint32_t &h0, uint32_t &h1, uint32_t &p0, uint32_t &p1, uint32_t &W) {
-            W = src[y][w];
-            const uint32_t Wp = w > 0 ? src[y][w - 1] : 0u;
-            const uint32_t Wn = w + 1 < NW ? src[y][w + 1] : 0u;
-            const uint32_t L = __funnelshift_l(Wp, W, 1), R = __funnelshift_r(W, Wn, 1);
-            h0 = L ^ W ^ R;
-            h1 = (L & W) | (L & R) | (W & R);
-            p0 = L ^ R;
-            p1 = L & R;
+    // ---- B: K generations with the state in registers.  Thread (band, w) owns
+    // bitmap word w of region rows [RB band, RB band + RB); horizontal neighbour
+    // words come by shuffle (lane +-1), the rows above / below the band through
+    // shared memory (one exchange per generation).  What enters at the region
+    // edges (the shuffle partners of words 0 and NW-1, rows past the staged
+    // region, idle lanes) is garbage that moves one cell per generation: after K
+    // generations it reaches column c0 - 1 on the left, c0 + 160 - 2K >= c0 + 144
+    // on the right and rows outside [K, K + rho) -- never a cell phase C writes.
+    // Cells outside the triangle are re-masked dead every generation (skipped
+    // when the whole warp's mask is all ones).
+    {
+        const int lane = t & 31;
+        const bool act = lane < BPW * NW;
+        const int w = act ? lane % NW : 0;
+        const int band = (t >> 5) * BPW + (act ? lane / NW : 0);
+        const bool live = act && band < NBAND;
+        uint32_t X[RB], Mk[RB];
+        // CTA-uniform: every region cell (rows r0-K .. r0+rho+K-1, bitmap columns
+        // cs .. cs+32 NW-1) inside the triangle and the domain -> no masks at all
+        const bool inside = cs >= 0 && cs + 32 * NW - 1 <= r0 - K && r0 + RHO + K <= a.n;
+        bool ones = true;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const int y = RB * band + q;
+            const bool in = live && y < NIN;
+            X[q] = in ? sm.A[y][w] : 0u;
+            Mk[q] = (in && !inside) ? tri_mask(r0 - K + y, a.n, cs + 32 * w) : 0xffffffffu;
+            ones = ones && Mk[q] == 0xffffffffu;
+        }
+        const bool nomask = inside || __all_sync(0xffffffffu, ones);
+        auto hsum = [&](uint32_t V, uint32_t &s0, uint32_t &s1, uint32_t &q0, uint32_t &q1) {
+            const uint32_t Vp = __shfl_up_sync(0xffffffffu, V, 1);
+            const uint32_t Vn = __shfl_down_sync(0xffffffffu, V, 1);
+            const uint32_t L = __funnelshift_l(Vp, V, 1), R = __funnelshift_r(V, Vn, 1);
+            s0 = L ^ V ^ R;                                   // 3-cell row sum (bit 0, bit 1)
+            s1 = (L & V) | (L & R) | (V & R);
+            q0 = L ^ R;                                       // 2-cell sum without the centre
+            q1 = L & R;
         };
-        if (ya < yb) {
-            uint32_t h0u, h1u, h0m, h1m, p0m, p1m, Wm, xx, yy;
-            terms(ya - 1, h0u, h1u, xx, yy, Wm);
-            terms(ya, h0m, h1m, p0m, p1m, Wm);
+        auto generations = [&](auto masked) {
 #pragma unroll 1
-            for (int y = ya; y < yb; ++y) {
-                uint32_t d0, d1, dp0, dp1, dW;
-                terms(y + 1, d0, d1, dp0, dp1, dW);
-                const uint32_t z0 = h0u ^ d0 ^ p0m;
-                const uint32_t k0 = (h0u & d0) | (h0u & p0m) | (d0 & p0m);
-                const uint32_t x = h1u ^ d1 ^ p1m;
-                const uint32_t ge2 = (h1u & d1) | (h1u & p1m) | (d1 & p1m);
-                dst[y][w] = (~ge2 & (x ^ k0)) & (z0 | Wm) & sm.M[y][w];
-                h0u = h0m; h1u = h1m;
-                h0m = d0; h1m = d1; p0m = dp0; p1m = dp1; Wm = dW;
+            for (int g = 0; g < K; ++g) {
+                const int pb = g & 1;
+                if (live) {
+                    sm.top[pb][band][w] = X[0];
+                    sm.bot[pb][band][w] = X[RB - 1];
+                }
+                __syncthreads();
+                const uint32_t up = (live && band > 0) ? sm.bot[pb][band - 1][w] : 0u;
+                const uint32_t dn = (live && band + 1 < NBAND) ? sm.top[pb][band + 1][w] : 0u;
+                uint32_t h0[RB + 2], h1[RB + 2], p0[RB], p1[RB], u0, u1;
+                hsum(up, h0[0], h1[0], u0, u1);
+#pragma unroll
+                for (int q = 0; q < RB; ++q) hsum(X[q], h0[q + 1], h1[q + 1], p0[q], p1[q]);
+                hsum(dn, h0[RB + 1], h1[RB + 1], u0, u1);
+#pragma unroll
+                for (int q = 0; q < RB; ++q) {
+                    // neighbour count = h(row above) + h(row below) + p(own row), bit-sliced
+                    const uint32_t a0 = h0[q], b0 = h0[q + 2], c0_ = p0[q];
+                    const uint32_t a1 = h1[q], b1 = h1[q + 2], c1 = p1[q];
+                    const uint32_t z0 = a0 ^ b0 ^ c0_;
+                    const uint32_t k0 = (a0 & b0) | (a0 & c0_) | (b0 & c0_);
+                    const uint32_t x = a1 ^ b1 ^ c1;
+                    const uint32_t ge2 = (a1 & b1) | (a1 & c1) | (b1 & c1);
+                    const uint32_t nx = (~ge2 & (x ^ k0)) & (z0 | X[q]);
+                    X[q] = decltype(masked)::value ? nx & Mk[q] : nx;
+                }
             }
+        };
+        if (nomask) generations(MaskTag<false>{});
+        else generations(MaskTag<true>{});
+        __syncthreads();                                      // last exchange read before A is overwritten
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const int y = RB * band + q;
+            if (live && y < NINMAX) sm.A[y][w] = X[q];
         }
         __syncthreads();
     }
-    uint32_t (*fin)[NW] = (K & 1) ? sm.B : sm.A;
+    uint32_t (*fin)[NW] = sm.A;
     // ---- C: aligned-chunk ownership (a 16-byte chunk is written by the tile
     // holding its first cell; the region covers the <= 15-column spill past the
     // tile for K <= 8).  Byte stores only where a chunk crosses a row boundary:
     // the row-i part of a chunk running past the row end (diagonal tiles), and
     // the head bytes of a row whose first chunk started in the previous row (c0 = 0).
-    constexpr int L = RHO / 16;
+    // A warp covers 4 rows x 8 chunk slots per pass (lane = 8 row + slot), so
+    // each warp store is four 128-byte runs.  A row segment of len <= rho cells
+    // starting at phase delta touches slots 0..7 only.
+    const int slot = t & 7;
+    // owned tile rows [rr_lo, rr_hi) and the row offset r0 - c0, in 32 bits
+    const int64_t lo64 = a.R0 - r0, hi64 = a.R1 - r0;
+    const int rr_lo = lo64 < 0 ? 0 : (lo64 > RHO ? RHO : (int)lo64);
+    const int rr_hi = hi64 < 0 ? 0 : (hi64 > RHO ? RHO : (int)hi64);
+    const int64_t dr64 = r0 - c0 + 1;                         // seg(rr) = dr + rr cells in the row from c0
+    const int dr = dr64 > (1 << 20) ? (1 << 20) : (dr64 < -RHO ? -RHO : (int)dr64);
 #pragma unroll 1
-    for (int idx = t; idx < RHO * SLOTS; idx += NT) {
-        const int rr = idx / SLOTS, q = idx % SLOTS;
-        const int64_t i = r0 + rr;
-        if (i >= a.R1 || i < a.R0) continue;
-        const int64_t seg = i - c0 + 1;
-        const int64_t len = seg < RHO ? seg : RHO;
-        if (len <= 0) continue;
+    for (int rr = (t >> 3) + rr_lo; rr < rr_hi; rr += NT / 8) {
+        const int seg = dr + rr;
+        if (seg <= 0) continue;
+        const int len = seg < RHO ? seg : RHO;
         const uint64_t s = sm.seg[rr];
         const int delta = (int)((0u - (uint32_t)s) & 15u);
         const int y = rr + K;
-        if (q == L) {                                          // head bytes of the row (c0 = 0 only)
-            if (c0 != 0) continue;
-            const int hb = delta < len ? delta : (int)len;
+        if (slot == 0 && c0 == 0) {                           // head bytes of the row (c0 = 0 only)
+            const int hb = delta < len ? delta : len;
 #pragma unroll 1
             for (int u = 0; u < hb; ++u) {
                 const int x = u + K;
                 a.out[s + u] = (uint8_t)((fin[y][x >> 5] >> (x & 31)) & 1u);
             }
-            continue;
         }
-        const int off = delta + 16 * q;
+        const int off = delta + 16 * slot;
         if (off >= len) continue;
-        const int64_t j0 = c0 + off;
         const int x = off + K;
-        if (j0 + 15 <= i) {
+        if (off + 16 <= seg) {
             const uint32_t w0 = fin[y][x >> 5];
             const uint32_t w1 = (x >> 5) + 1 < NW ? fin[y][(x >> 5) + 1] : 0u;
             const uint32_t b = __funnelshift_r(w0, w1, (uint32_t)(x & 31));
@@ -872,7 +915,7 @@ __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, 
                       bits::spread4((b >> 8) & 15u), bits::spread4((b >> 12) & 15u));
         } else {                                               // crosses the row end: row-i part only
 #pragma unroll 1
-            for (int u = 0; u <= (int)(i - j0); ++u) {
+            for (int u = 0; u < seg - off; ++u) {
                 const int xu = x + u;
                 a.out[s + off + u] = (uint8_t)((fin[y][xu >> 5] >> (xu & 31)) & 1u);
             }
@@ -885,25 +928,18 @@ __global__ void __launch_bounds__(NT) ca_multi_kernel(CaArgs a) {
     __shared__ __align__(16) Smem sm;
     if (STRAT == TRI_BB) {
         if (blockIdx.x > blockIdx.y + (uint32_t)a.tile_row_begin) return;
-    }
-    if (threadIdx.x == 0) bits::mbar_init(&sm.bar, NINMAX);
-    __syncthreads();
-    if (STRAT == TRI_BB) {
-        tile(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm, 0u);
+        tile(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm);
     } else if (STRAT == TRI_LAMBDA) {
         const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
         if (w >= a.omega_end) return;
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
-        tile(a, bi, bj, sm, 0u);
+        tile(a, bi, bj, sm);
     } else {
-        uint32_t parity = 0;
 #pragma unroll 1
         for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
-            tile(a, t.bi, t.bj, sm, parity);
-            parity ^= 1u;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
+            tile(a, t.bi, t.bj, sm);
+            __syncthreads();                                  // smem reused by the next tile
         }
     }
 }

@@ -1,6 +1,6 @@
 """Run one hot-path kernel a few times (for ncu captures and quick sweeps).
 
-python tools/run_one.py edm|dummy|collide|ca|triplet [--rho R] [--strategy S] [--reps K] [--n N]
+python tools/run_one.py edm|dummy|collide|ca|ca_steps|triplet [--rho R] [--strategy S] [--reps K] [--n N]
 Prints per-launch CUDA-event times (ms).  Product path only (no oracle)."""
 import argparse
 import os
@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--strategy", default="persist")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--k", type=int, default=8)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     w = a.workload
@@ -45,6 +46,12 @@ def main():
         x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
         y = torch.empty_like(x)
         fn = lambda: tri.tri_ca_step(m, a.strategy, x, y)
+    elif w == "ca_steps":
+        n = a.n or 32768
+        m = tri.tri_map_init(n, 128)
+        x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
+        y = torch.empty_like(x)
+        fn = lambda: tri.tri_ca_steps(m, a.strategy, a.k, x, y)
     elif w == "triplet":
         n = a.n or 4096
         m = tri.tet_map_init(n, a.rho or 16)
