@@ -371,66 +371,11 @@ __device__ __forceinline__ uint32_t pack32(const uint4 lo, const uint4 hi) {
 // 4 bits -> 4 bytes {0,1}: nibble * 0x00204081 puts bit q at 8q (no collisions).
 __device__ __forceinline__ uint32_t spread4(uint32_t v) { return (v * 0x00204081u) & 0x01010101u; }
 
-// Staged halo rows (rho = 128): each row's 16-byte-aligned byte range is copied
-// into shared memory with coalesced cp.async (LDGSTS, 16 bytes per lane, the
-// whole CTA streaming chunk after chunk), then packed to bits from shared
-// memory.  Row stride 16 (mod 128) bytes keeps the per-thread LDS.128 reads of
-// 8 consecutive rows conflict-free.  (One cp.async.bulk per row was tried: its
-// per-lane uniform-register serialisation cost ~8 issue slots per row.)
 template <int RHO>
-struct Stage {
-    static constexpr bool kOn = RHO == 128;
-    static constexpr int RAWB = 32 * (Cfg<RHO>::NW + 1);     // bytes staged per row (2 chunks per word + 1)
-    static constexpr int NCH = RAWB / 16;
-    static constexpr int STRIDE = RAWB + 16;                   // = 16 (mod 128) for RHO = 128
-};
-
-template <int RHO, bool STAGED = Stage<RHO>::kOn>
 struct Smem {
     uint32_t in[Cfg<RHO>::NIN][Cfg<RHO>::NW];
     uint32_t out[RHO][Cfg<RHO>::NW];
 };
-template <int RHO>
-struct Smem<RHO, true> {
-    uint32_t in[Cfg<RHO>::NIN][Cfg<RHO>::NW];
-    uint32_t out[RHO][Cfg<RHO>::NW];
-    alignas(16) uint8_t raw[Cfg<RHO>::NIN][Stage<RHO>::STRIDE];
-    uint64_t seg[RHO];                        // local packed offset of (r0 + rr, c0), phase C
-    alignas(8) unsigned long long bar;        // TMA completion barrier
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// TMA 1-D bulk copy global -> shared, completion counted on the mbarrier.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
 
 // Byte mask of chunk bytes [lo, hi) (clamped to the 16-byte chunk) applied in place.
 __device__ __forceinline__ uint32_t word_mask(int64_t lo_c, int64_t hi_c, int u) {
@@ -443,62 +388,6 @@ __device__ __forceinline__ void mask_chunk(uint4 &c, int64_t lo_c, int64_t hi_c)
     c.y &= word_mask(lo_c, hi_c, 1);
     c.z &= word_mask(lo_c, hi_c, 2);
     c.w &= word_mask(lo_c, hi_c, 3);
-}
-
-// Phase A with TMA staging: thread t = input row t resolves the row (slice /
-// halo / dead; whole window inside the row or not), issues one cp.async.bulk
-// for a whole row or stages a boundary row itself with byte masks, waits on
-// the CTA's mbarrier, then packs its staged bytes to bits.
-template <int RHO>
-__device__ __forceinline__ void phase_a_tma(const CaArgs &a, int64_t r0, int64_t c0, Smem<RHO, true> &sm,
-                                            uint32_t parity) {
-    constexpr int NW = Cfg<RHO>::NW, NIN = Cfg<RHO>::NIN;
-    constexpr int RAWB = Stage<RHO>::RAWB, NCH = Stage<RHO>::NCH;
-    const int t = threadIdx.x;
-    if (t >= NIN) return;
-    const int64_t r = r0 - 1 + t;
-    uint8_t *dst = sm.raw[t];
-    const uint8_t *p = row_ptr(a, r);
-    uint32_t e = 0;
-    if (t >= 1 && t <= RHO) sm.seg[t - 1] = tri::T2((uint64_t)(r0 + t - 1)) + (uint64_t)c0 - a.base;
-    if (!p) {
-#pragma unroll
-        for (int h = 0; h < NCH; ++h) *reinterpret_cast<uint4 *>(dst + 16 * h) = make_uint4(0, 0, 0, 0);
-        mbar_arrive(&sm.bar);
-    } else {
-        const int64_t cs = c0 - 1;
-        const uintptr_t A = (uintptr_t)(p + cs);
-        e = (uint32_t)(A & 15u);
-        const int64_t col0 = cs - (int64_t)e;
-        const uint4 *q = (const uint4 *)(A & ~(uintptr_t)15);
-        if (col0 >= 0 && col0 + RAWB - 1 <= r) {             // whole range inside the row: one TMA copy
-            mbar_arrive_tx(&sm.bar, RAWB);
-            bulk_g2s(dst, q, RAWB, &sm.bar);
-        } else {                                              // boundary row: masked manual staging
-#pragma unroll
-            for (int h = 0; h < NCH; ++h) {
-                const int64_t cb = col0 + 16 * h;
-                const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
-                uint4 c = make_uint4(0, 0, 0, 0);
-                if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
-                    c = __ldg(q + h);
-                    mask_chunk(c, lo_c, hi_c);
-                }
-                *reinterpret_cast<uint4 *>(dst + 16 * h) = c;
-            }
-            mbar_arrive(&sm.bar);
-        }
-    }
-    mbar_wait(&sm.bar, parity);
-    uint32_t prev = 0;
-#pragma unroll
-    for (int v = 0; v <= NW; ++v) {
-        const uint32_t lo = pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v));
-        const uint32_t hi = pack16(*reinterpret_cast<const uint4 *>(dst + 32 * v + 16));
-        const uint32_t P = lo | (hi << 16);
-        if (v > 0) sm.in[t][v - 1] = __funnelshift_r(prev, P, e);
-        prev = P;
-    }
 }
 
 template <int RHO>
@@ -559,17 +448,12 @@ __device__ __forceinline__ void phase_a_row(const CaArgs &a, int64_t r, int64_t 
 }
 
 template <int RHO>
-__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem<RHO> &sm, uint32_t parity) {
+__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem<RHO> &sm) {
     constexpr int NIN = Cfg<RHO>::NIN, NW = Cfg<RHO>::NW, NT = Cfg<RHO>::NT, NBAND = Cfg<RHO>::NBAND;
     const int t = threadIdx.x;
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
     // ---- A: rows r0-1 .. r0+RHO -> bitmaps (one row per thread)
-    if constexpr (Stage<RHO>::kOn) {
-        phase_a_tma<RHO>(a, r0, c0, sm, parity);
-    } else {
-        (void)parity;
-        if (t < NIN) phase_a_row<RHO>(a, r0 - 1 + t, c0, sm.in[t]);
-    }
+    if (t < NIN) phase_a_row<RHO>(a, r0 - 1 + t, c0, sm.in[t]);
     __syncthreads();
     // ---- B: B3/S23 on words; thread = (word w, band of 8 output rows)
     {
@@ -615,9 +499,7 @@ __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, 
         const int rr = idx / L, k = idx % L;
         const int64_t i = r0 + rr;
         if (i >= a.R1 || i < a.R0) continue;
-        uint64_t s;
-        if constexpr (Stage<RHO>::kOn) s = sm.seg[rr];        // computed once per row in phase A
-        else s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.base;
+        const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.base;
         const int64_t seg = i - c0 + 1;
         const int64_t len = seg < RHO ? seg : RHO;
         const int off = (int)((0u - (uint32_t)s) & 15u) + 16 * k;
@@ -646,26 +528,18 @@ __global__ void __launch_bounds__(Cfg<RHO>::NT) ca_bits_kernel(CaArgs a) {
         const uint32_t bi = blockIdx.y + (uint32_t)a.tile_row_begin;
         if (bj > bi) return;
     }
-    if constexpr (Stage<RHO>::kOn) {
-        if (threadIdx.x == 0) mbar_init(&sm.bar, Cfg<RHO>::NIN);
-        __syncthreads();
-    }
     if (STRAT == TRI_BB) {
-        tile<RHO>(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm, 0u);
+        tile<RHO>(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm);
     } else if (STRAT == TRI_LAMBDA) {
         const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
         if (w >= a.omega_end) return;
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
-        tile<RHO>(a, bi, bj, sm, 0u);
+        tile<RHO>(a, bi, bj, sm);
     } else {
-        uint32_t parity = 0;
 #pragma unroll 1
         for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
-            tile<RHO>(a, t.bi, t.bj, sm, parity);
-            parity ^= 1u;
-            // generic-proxy reads of the staging buffer before the next tile's TMA writes
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tile<RHO>(a, t.bi, t.bj, sm);
             __syncthreads();                                  // smem reused by the next tile
         }
     }
@@ -701,11 +575,11 @@ tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
 }  // namespace bits
 
 // ============================================================================
-// k generations per launch (temporal blocking with deep halos):
-// rho = 128 tiles; the CTA stages rows [r0-k, r0+rho+k) x columns
-// [c0-k, c0+rho+k) (TMA bulk copies), packs them to bitmaps, runs k
-// generations in shared memory -- re-masking the triangle after each one --
-// and writes only its own row segments [c0, min(c0+rho, i+1)): aligned chunks
+// k generations per launch (temporal blocking with deep halos);
+// also tri_ca_step at rho = 128 (k = 1).  rho = 128 tiles; the CTA loads rows
+// [r0-k, r0+rho+k) x columns [c0-k, c0+rho+k), packs them to bitmaps, runs k
+// generations with the bitmap in registers -- re-masking the triangle after
+// each one -- and writes only its own row segments [c0, min(c0+rho, i+1)): aligned chunks
 // with 16-byte streaming stores, the partial chunks at segment ends byte-wise
 // (a neighbouring tile writes the other bytes of such a chunk).  Garbage from
 // the region edge moves one cell per generation, so after k generations the
