@@ -19,10 +19,19 @@ namespace tri {
 TRI_HD uint64_t T2(uint64_t r) { return r * (r + 1) / 2; }
 TRI_HD uint64_t T3(uint64_t r) { return r * (r + 1) * (r + 2) / 6; }
 
-// fp32 estimate of sqrt(x): MUFU.RSQ on the device, libm on the host.
+// Bare MUFU.RSQ: rsqrtf() adds a denormal-input rescale (FSETP + 2 FMUL + FSEL)
+// around it; for normal inputs the MUFU result is the same.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// fp32 estimate of sqrt(x): MUFU.RSQ on the device, libm on the host.  x = 8 w + 1
+// >= 1 is never denormal.
 TRI_HD float sqrt_est(float x) {
 #ifdef __CUDA_ARCH__
-    return x * rsqrtf(x);   // MUFU.RSQ + FMUL (lambda_R form)
+    return x * rsqrt_ftz(x);   // MUFU.RSQ + FMUL (lambda_R form)
 #else
     return sqrtf(x);
 #endif
@@ -130,9 +139,11 @@ TRI_HD void tet_map(uint64_t w, uint32_t &i, uint32_t &j, uint32_t &k) {
 // omega chunk [begin + c*q + min(c, r), ...) of the balanced split of
 // [begin, end) (q = nb / grid, r = nb % grid), evaluates lambda ONCE at the
 // chunk start and then steps with the Eq. 1 successor rule (j + 1, wrapping to
-// (i + 1, 0) past the diagonal).  Consecutive tiles -- and the output rows they
-// share -- stay in one CTA, so the straddling 32-B sectors are completed while
-// still in L2 (a grid-stride loop scatters them across CTAs that drift apart).
+// (i + 1, 0) past the diagonal).  Measured on B200: it wins where CTA launch is
+// the cost (dummy kernel, n = 65536: 3.05 vs 6.25 ms) and loses on the
+// HBM-write-bound kernels, whose packed rows end in the diagonal tile and
+// resume in tile (i, 0) -- bi tiles earlier in omega, so in another CTA at
+// another time -- leaving partial 32-B sectors to be read back from DRAM.
 struct TileWalk {
     uint64_t w, end;
     uint32_t bi, bj;

@@ -50,7 +50,7 @@ __device__ __forceinline__ float atm(float a, float b, float c) {
     const float abc = a * b * c;
     const float bc = b + c, dbc = b - c;
     const float P = (bc - a) * (a - dbc) * (a + dbc);
-    const float r = rsqrtf(abc);
+    const float r = tri::rsqrt_ftz(abc);         // abc < 2^-126 overflows E (r^9) anyway
     const float r2 = r * r;
     const float r3 = r2 * r;
     return fmaf(0.375f * P * r2, r3, r3);
@@ -283,7 +283,9 @@ __device__ __forceinline__ f2 atm2(f2 aa, f2 a2, f2 na375, f2 c375, f2 one, f2 b
     const f2 P = mul2(u, t);
     float x0, x1;
     upk(mul2(mul2(b, c), aa), x0, x1);
-    const f2 r = pk(rsqrtf(x0), rsqrtf(x1));
+    // bare MUFU.RSQ (no denormal rescale): abc < 2^-126 would give E = r^9 > 2^567,
+    // an fp32 overflow (inf) either way
+    const f2 r = pk(tri::rsqrt_ftz(x0), tri::rsqrt_ftz(x1));
     const f2 r2 = mul2(r, r);
     const f2 y = fma2(P, r2, one);
     return mul2(mul2(r2, r), y);
