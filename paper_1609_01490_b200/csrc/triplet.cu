@@ -272,14 +272,14 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
     return r;
 }
 
-// Two ATM energies (without nu) for the s-pair (b, c) at fixed a, 11 FP32 ops each:
-//   P' = 3/8 P = (0.375 (b + c) - 0.375 a) * (a^2 - (b - c)^2)
-//   E  = r^3 (1 + P' r^2),  r = rsqrt(a b c)      (a^2 and -0.375 a hoisted per q)
-__device__ __forceinline__ f2 atm2(f2 aa, f2 a2, f2 na375, f2 c375, f2 one, f2 b, f2 c) {
+// Two ATM energies (without nu) for the s-pair (b, c) at fixed a, 10 FP32 ops each:
+//   P' = 3/8 P = (0.375 a - 0.375 (b + c)) * ((b - c)^2 - a^2)     (both factors negated)
+//   E  = r^3 (1 + P' r^2),  r = rsqrt(a b c)      (0.375 a and -a^2 hoisted per q)
+// Returns E as the product r3 * y so the caller can fuse it into its accumulators.
+__device__ __forceinline__ void atm2(f2 aa, f2 na2, f2 a375, f2 nc375, f2 one, f2 b, f2 c, f2 &r3, f2 &y) {
     const f2 sg = add2(b, c), dl = sub2(b, c);
-    const f2 u = fma2(c375, sg, na375);
-    const f2 ndl = dl ^ 0x8000000080000000ull;          // -(b - c), both lanes (sign flip, no FP op)
-    const f2 t = fma2(ndl, dl, a2);
+    const f2 u = fma2(nc375, sg, a375);                  // 0.375 (a - b - c)
+    const f2 t = fma2(dl, dl, na2);                       // (b - c)^2 - a^2
     const f2 P = mul2(u, t);
     float x0, x1;
     upk(mul2(mul2(b, c), aa), x0, x1);
@@ -287,8 +287,8 @@ __device__ __forceinline__ f2 atm2(f2 aa, f2 a2, f2 na375, f2 c375, f2 one, f2 b
     // an fp32 overflow (inf) either way
     const f2 r = pk(tri::rsqrt_ftz(x0), tri::rsqrt_ftz(x1));
     const f2 r2 = mul2(r, r);
-    const f2 y = fma2(P, r2, one);
-    return mul2(mul2(r2, r), y);
+    y = fma2(P, r2, one);
+    r3 = mul2(r2, r);
 }
 
 struct WarpSmem {
@@ -347,7 +347,7 @@ __device__ __forceinline__ void tile(const TripArgs &a, WarpSmem &sm, uint32_t k
     }
     __syncwarp();
     const int64_t p = (int64_t)kb * 32 + lane;
-    const f2 c375 = pk(0.375f, 0.375f), one = pk(1.f, 1.f);
+    const f2 nc375 = pk(-0.375f, -0.375f), one = pk(1.f, 1.f);
     f2 es[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) es[t] = 0ull;
@@ -355,17 +355,19 @@ __device__ __forceinline__ void tile(const TripArgs &a, WarpSmem &sm, uint32_t k
 #pragma unroll 1
     for (int q = 0; q < 32; ++q) {
         const float av = sm.Dpq[lane][q];
-        const f2 aa = pk(av, av), na = pk(-0.375f * av, -0.375f * av), a2 = pk(av * av, av * av);
-        f2 row = 0ull;
+        const f2 aa = pk(av, av), a375 = pk(0.375f * av, 0.375f * av), na2 = pk(-av * av, -av * av);
+        f2 row = 0ull, row2 = 0ull;
         bool pq_ok = true;
         if (MASKED) pq_ok = p < a.n && (kb != ib || lane > q) && ((int64_t)ib * 32 + q < a.n);
 #pragma unroll
         for (int s4 = 0; s4 < 8; ++s4) {
             const float4 b4 = *reinterpret_cast<const float4 *>(&sm.Dqs[q][4 * s4]);
             const float4 c4 = *reinterpret_cast<const float4 *>(&sm.Dps[lane][4 * s4]);
-            f2 e01 = atm2(aa, a2, na, c375, one, pk(b4.x, b4.y), pk(c4.x, c4.y));
-            f2 e23 = atm2(aa, a2, na, c375, one, pk(b4.z, b4.w), pk(c4.z, c4.w));
+            f2 r01, y01, r23, y23;
+            atm2(aa, na2, a375, nc375, one, pk(b4.x, b4.y), pk(c4.x, c4.y), r01, y01);
+            atm2(aa, na2, a375, nc375, one, pk(b4.z, b4.w), pk(c4.z, c4.w), r23, y23);
             if (MASKED) {
+                f2 e01 = mul2(r01, y01), e23 = mul2(r23, y23);
                 float e0, e1, e2, e3;
                 upk(e01, e0, e1);
                 upk(e23, e2, e3);
@@ -378,13 +380,20 @@ __device__ __forceinline__ void tile(const TripArgs &a, WarpSmem &sm, uint32_t k
                 e3 = (pq_ok && sg + 3 < a.n && (sj || sb + 3 < q)) ? e3 : 0.f;
                 e01 = pk(e0, e1);
                 e23 = pk(e2, e3);
+                row = add2(row, e01);
+                row2 = add2(row2, e23);
+                es[2 * s4] = add2(es[2 * s4], e01);
+                es[2 * s4 + 1] = add2(es[2 * s4 + 1], e23);
+            } else {
+                // E = r3 y fused into both accumulators
+                row = fma2(r01, y01, row);
+                row2 = fma2(r23, y23, row2);
+                es[2 * s4] = fma2(r01, y01, es[2 * s4]);
+                es[2 * s4 + 1] = fma2(r23, y23, es[2 * s4 + 1]);
             }
-            row = add2(row, add2(e01, e23));
-            es[2 * s4] = add2(es[2 * s4], e01);
-            es[2 * s4 + 1] = add2(es[2 * s4 + 1], e23);
         }
         float r0, r1;
-        upk(row, r0, r1);
+        upk(add2(row, row2), r0, r1);
         const float rs = r0 + r1;          // sum over s of E(p, q, s) for this lane's p
         accp += rs;
         float tq = rs;                     // sum over p (lanes) -> e_q
