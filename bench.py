@@ -451,6 +451,20 @@ def bench_triplet(rank, world, pk):
     res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "TFLOP/s (fp32 ops)",
                        "frac": round(ach / peak, 4), "ops_per_triplet": 12, "mufu_per_triplet": 1}
     res["tiles"] = {"tet": tri.tet_map_init(n, 32).blocks, "bb3d": 128 ** 3}
+    # succinct lookup table vs cube root for the tetrahedral layer: map evaluations
+    # per second (two maps + the Eq./successor checks per omega) over every tile of n = 4096 at
+    # rho = 8 (512 layers, 22,500,864 tiles)
+    if rank == 0:
+        kmax, shift = 511, 12
+        cnt = (kmax + 1) * (kmax + 2) * (kmax + 3) // 6 - 1
+        fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+        lut = torch.empty(tri.tet_lut_bytes(kmax, shift), dtype=torch.uint8, device="cuda")
+        tri.tet_lut_build(kmax, shift, lut)
+        tc, _ = time_steps(lambda: tri.tet_map_eval(0, cnt, None, fail), 5, 2, 1)
+        tl, _ = time_steps(lambda: tri.tet_map_eval_lut(0, cnt, kmax, shift, lut, None, fail), 5, 2, 1)
+        res["tet_map"] = {"tiles": cnt, "lut_bytes": lut.numel(), "shift": shift,
+                          "cbrt_maps_per_s": 2 * cnt / (tc / 5 * 1e-3), "lut_maps_per_s": 2 * cnt / (tl / 5 * 1e-3),
+                          "speedup_lut": round(tc / tl, 3)}
     return {"config": "ATM triplet energies on the tetrahedral map, n=4096 fp32", "metric": "triplets/s",
             "value": trip / (best * 1e-3), **res}
 

@@ -234,6 +234,23 @@ tri_status tet_lambda(uint64_t omega, uint32_t *i, uint32_t *j, uint32_t *k);
 tri_status tet_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ijk,
                         unsigned long long *d_fail, void *stream);
 
+/* Succinct lookup table for the tetrahedral layer index ("a succint
+ * lookup table of o(T_n) combined with coordinate computations"; it deliberately
+ * relaxes the paper's no-extra-data condition, P:405-410 -- SURVEY 8(f)4).
+ * Layers k = 0..kmax.  Layout of the caller-owned device buffer (8-byte aligned):
+ *   S[k] = T3(k), k = 0..kmax+1                                  (uint64)
+ *   G[g] = max{k : T3(k) <= g * 2^shift}, g = 0..nb, nb = (T3(kmax+1) >> shift) + 1  (uint32)
+ * k(omega) = the largest k in [G[g], G[g+1]] with S[k] <= omega, g = omega >> shift
+ * (a bisection over the few layers of one bucket), then (i, j) = lambda(omega - S[k]):
+ * loads instead of the cube root.  shift in [0, 40]; 0 < kmax < 2^20.
+ * tet_lut_bytes: buffer size (0 on bad arguments).  tet_lut_build: fills the buffer on
+ * the stream.  tet_map_eval_lut: tet_map_eval with the table-based map; requires
+ * omega0 + count < T3(kmax+1) (TRI_ERANGE otherwise). */
+size_t tet_lut_bytes(uint32_t kmax, int32_t shift);
+tri_status tet_lut_build(uint32_t kmax, int32_t shift, void *d_lut, size_t lut_bytes, void *stream);
+tri_status tet_map_eval_lut(uint64_t omega0, uint64_t count, uint32_t kmax, int32_t shift, const void *d_lut,
+                            uint32_t *d_ijk, unsigned long long *d_fail, void *stream);
+
 /* Triplet-interaction n-body on the tetrahedral map (
  * interaction = Axilrod-Teller-Muto, reading Q15): for every
  * triplet p > q > s in this rank's tiles, E = nu (1 + 3P/(8abc)) / (abc)^(3/2)

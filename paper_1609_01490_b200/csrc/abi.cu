@@ -251,6 +251,29 @@ tri_status tet_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ijk, unsign
     return launch_tet_map_eval(omega0, count, d_ijk, d_fail, (cudaStream_t)stream);
 }
 
+size_t tet_lut_bytes(uint32_t kmax, int32_t shift) {
+    if (kmax == 0 || kmax >= (1u << 20) || shift < 0 || shift > 40) return 0;
+    const uint64_t nb = (T3((uint64_t)kmax + 1) >> shift) + 1;
+    return (size_t)(8ull * ((uint64_t)kmax + 2) + 4ull * (nb + 1));
+}
+
+tri_status tet_lut_build(uint32_t kmax, int32_t shift, void *d_lut, size_t lut_bytes, void *stream) {
+    g_launches = 0;
+    const size_t need = tet_lut_bytes(kmax, shift);
+    if (!need || !d_lut || lut_bytes < need || ((uintptr_t)d_lut & 7u)) return TRI_EINVAL;
+    return launch_tet_lut_build(kmax, shift, d_lut, (cudaStream_t)stream);
+}
+
+tri_status tet_map_eval_lut(uint64_t omega0, uint64_t count, uint32_t kmax, int32_t shift, const void *d_lut,
+                            uint32_t *d_ijk, unsigned long long *d_fail, void *stream) {
+    g_launches = 0;
+    if (!d_fail || !d_lut || !tet_lut_bytes(kmax, shift) || ((uintptr_t)d_lut & 7u)) return TRI_EINVAL;
+    if (d_ijk && count >= (1ull << 30)) return TRI_EINVAL;
+    const uint64_t end = T3((uint64_t)kmax + 1);              // omega + 1 is mapped too
+    if (omega0 >= end || count > end - 1 - omega0) return TRI_ERANGE;
+    return launch_tet_map_eval_lut(omega0, count, kmax, shift, d_lut, d_ijk, d_fail, (cudaStream_t)stream);
+}
+
 tri_status tet_triplet(const tet_map_t *map, int32_t strategy, const float *d_pts4, double nu,
                        double *d_energy, void *stream) {
     g_launches = 0;

@@ -82,6 +82,73 @@ __global__ void __launch_bounds__(256) variant_scan_kernel(int variant, uint64_t
     }
 }
 
+// ---- succinct layer table: S[k] = T3(k), G[g] = max{k : T3(k) <= g << shift}
+struct TetLut {
+    const uint64_t *S;
+    const uint32_t *G;
+    int shift;
+};
+
+__host__ __device__ __forceinline__ TetLut lut_view(const void *d, uint32_t kmax, int shift) {
+    TetLut L;
+    L.S = (const uint64_t *)d;
+    L.G = (const uint32_t *)(L.S + (uint64_t)kmax + 2);
+    L.shift = shift;
+    return L;
+}
+
+// layer k from the table: bisection over [G[g], G[g+1]] on S (no cube root)
+__device__ __forceinline__ void tet_map_lut(const TetLut &L, uint64_t w, uint32_t &i, uint32_t &j, uint32_t &k) {
+    const uint64_t g = w >> L.shift;
+    uint32_t lo = __ldg(L.G + g), hi = __ldg(L.G + g + 1);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(L.S + mid) <= w) lo = mid;
+        else hi = mid - 1;
+    }
+    k = lo;
+    tri::lambda_map(w - __ldg(L.S + lo), i, j);
+}
+
+__global__ void __launch_bounds__(256) tet_lut_build_kernel(uint32_t kmax, int shift, uint64_t *S, uint32_t *G,
+                                                            uint64_t nb) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= (uint64_t)kmax + 1; t += stride)
+        S[t] = tri::T3(t);
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= nb; g += stride) {
+        const uint64_t w = g << shift;
+        uint32_t lo = 0, hi = kmax + 1;                       // largest k <= kmax + 1 with T3(k) <= w
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (tri::T3(mid) <= w) lo = mid;
+            else hi = mid - 1;
+        }
+        G[g] = lo;
+    }
+}
+
+__global__ void __launch_bounds__(256) tet_eval_lut_kernel(uint64_t w0, uint64_t count, TetLut L, uint32_t *ijk,
+                                                           unsigned long long *fail) {
+    unsigned long long bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+        const uint64_t w = w0 + t;
+        uint32_t i, j, k;
+        tet_map_lut(L, w, i, j, k);
+        const uint64_t Tk = tri::T3(k);
+        bool ok = (Tk <= w) && (w < tri::T3((uint64_t)k + 1)) && (j <= i) && (i <= k) &&
+                  (Tk + tri::T2(i) + j == w);
+        uint32_t i2, j2, k2;
+        tet_map_lut(L, w + 1, i2, j2, k2);
+        ok = ok && ((k2 == k && i2 == i && j2 == j + 1) || (k2 == k && i2 == i + 1 && j2 == 0) ||
+                    (k2 == k + 1 && i2 == 0 && j2 == 0));
+        bad += ok ? 0 : 1;
+        if (ijk) { ijk[3 * t] = i; ijk[3 * t + 1] = j; ijk[3 * t + 2] = k; }
+    }
+    bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(fail, bad);
+}
+
 unsigned eval_grid(uint64_t count) {
     uint64_t want = (count + 255) / 256;
     uint64_t cap = (uint64_t)tri::sm_count() * 8ull * 16ull;
@@ -117,6 +184,25 @@ tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk, uns
     if (cudaMemsetAsync(d_fail, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
     if (count == 0) return TRI_OK;
     tet_eval_kernel<<<eval_grid(count), 256, 0, st>>>(w0, count, d_ijk, d_fail);
+    note_launches(1);
+    return cuda_status();
+}
+
+tri_status launch_tet_lut_build(uint32_t kmax, int shift, void *d_lut, cudaStream_t st) {
+    uint64_t *S = (uint64_t *)d_lut;
+    uint32_t *G = (uint32_t *)(S + (uint64_t)kmax + 2);
+    const uint64_t nb = (T3((uint64_t)kmax + 1) >> shift) + 1;
+    const uint64_t n = nb > (uint64_t)kmax + 2 ? nb : (uint64_t)kmax + 2;
+    tet_lut_build_kernel<<<eval_grid(n), 256, 0, st>>>(kmax, shift, S, G, nb);
+    note_launches(1);
+    return cuda_status();
+}
+
+tri_status launch_tet_map_eval_lut(uint64_t w0, uint64_t count, uint32_t kmax, int shift, const void *d_lut,
+                                   uint32_t *d_ijk, unsigned long long *d_fail, cudaStream_t st) {
+    if (cudaMemsetAsync(d_fail, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
+    if (count == 0) return TRI_OK;
+    tet_eval_lut_kernel<<<eval_grid(count), 256, 0, st>>>(w0, count, lut_view(d_lut, kmax, shift), d_ijk, d_fail);
     note_launches(1);
     return cuda_status();
 }

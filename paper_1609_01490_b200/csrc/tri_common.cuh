@@ -120,11 +120,26 @@ TRI_HD bool rb_map(int64_t x, int64_t y, int64_t n, int64_t &i, int64_t &j) {
 }
 
 // Tetrahedral map: k = largest layer with T3(k) <= omega from an
-// fp32 cube-root estimate of (6 omega) (the real root y = x + 1 of
+// fp32 cube-root estimate of (6 omega) (device: MUFU lg2/ex2, host: cbrtf) (the real root y = x + 1 of
 // y^3 - y = 6 omega, reading Q13) plus one integer correction
 // step each way; then (i, j) = lambda(omega - T3(k)).
+// Device cube root as 2^(log2(x)/3) with the MUFU LG2 / EX2 approximations (relative
+// error ~2^-21, far inside the +-1 row the integer correction absorbs; x = 0 gives
+// 2^-inf = 0).  cbrtf() spends ~30 instructions on an exactly rounded result the
+// correction does not need.
+__device__ __forceinline__ float cbrt_est(float x) {
+    float l, y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(l * (1.0f / 3.0f)));
+    return y;
+}
+
 TRI_HD void tet_map(uint64_t w, uint32_t &i, uint32_t &j, uint32_t &k) {
+#ifdef __CUDA_ARCH__
+    const float c = cbrt_est((float)(6ull * w));
+#else
     const float c = cbrtf((float)(6ull * w));
+#endif
     float e = c - 1.0f;
     e = e > 0.0f ? e : 0.0f;
     uint32_t kk = (uint32_t)e;
@@ -262,6 +277,9 @@ tri_status launch_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ij, unsigned
                            cudaStream_t st);
 tri_status launch_tet_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ijk,
                                unsigned long long *d_fail, cudaStream_t st);
+tri_status launch_tet_lut_build(uint32_t kmax, int shift, void *d_lut, cudaStream_t st);
+tri_status launch_tet_map_eval_lut(uint64_t w0, uint64_t count, uint32_t kmax, int shift, const void *d_lut,
+                                   uint32_t *d_ijk, unsigned long long *d_fail, cudaStream_t st);
 tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
                                unsigned long long *d_first, cudaStream_t st);
 tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream_t st);

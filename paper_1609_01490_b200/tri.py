@@ -78,6 +78,9 @@ SIGNATURES = {
     "tet_map_init": ([ctypes.POINTER(TetMap), c_i64, c_i32, c_i32, c_i32], c_i32),
     "tet_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
     "tet_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
+    "tet_lut_bytes": ([c_u32, c_i32], ctypes.c_size_t),
+    "tet_lut_build": ([c_u32, c_i32, c_vp, ctypes.c_size_t, c_vp], c_i32),
+    "tet_map_eval_lut": ([c_u64, c_u64, c_u32, c_i32, c_vp, c_vp, c_vp, c_vp], c_i32),
     "tet_triplet": ([ctypes.POINTER(TetMap), c_i32, c_vp, ctypes.c_double, c_vp, c_vp], c_i32),
     "tri_last_launch_count": ([], c_i32),
     "tri_status_str": ([c_i32], ctypes.c_char_p),
@@ -179,6 +182,21 @@ def tet_lambda(omega):
 
 def tet_map_eval(omega0, count, d_ijk, d_fail, stream=None):
     _ok(lib().tet_map_eval(omega0, count, _ptr(d_ijk), _ptr(d_fail), _stream(stream)), "tet_map_eval")
+
+
+def tet_lut_bytes(kmax, shift):
+    """Bytes of the succinct layer table (0 on bad arguments); host-only arithmetic."""
+    return int(lib().tet_lut_bytes(kmax, shift))
+
+
+def tet_lut_build(kmax, shift, d_lut, stream=None):
+    nb = _nbytes(d_lut) if d_lut is not None else 0
+    _ok(lib().tet_lut_build(kmax, shift, _ptr(d_lut), nb, _stream(stream)), "tet_lut_build")
+
+
+def tet_map_eval_lut(omega0, count, kmax, shift, d_lut, d_ijk, d_fail, stream=None):
+    _ok(lib().tet_map_eval_lut(omega0, count, kmax, shift, _ptr(d_lut), _ptr(d_ijk), _ptr(d_fail),
+                               _stream(stream)), "tet_map_eval_lut")
 
 
 # ----------------------------------------------------------------------------- kernels

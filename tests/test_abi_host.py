@@ -152,3 +152,18 @@ def test_host_lambda_nodiag_vs_oracle(L, orc):
     for w in (2**39, 2**40 - 1):
         i, j = tri.tri_lambda_nodiag(w)
         assert i * (i - 1) // 2 <= w < i * (i + 1) // 2 and j == w - i * (i - 1) // 2
+
+
+def test_tet_lut_bytes(L):
+    """Succinct layer table size: 8 (kmax + 2) + 4 (nb + 1), nb = (T3(kmax+1) >> shift) + 1."""
+    def t3(k):
+        return k * (k + 1) * (k + 2) // 6
+    for kmax, shift in [(1, 0), (119, 4), (511, 13), (4000, 20), (2 ** 20 - 1, 40)]:
+        nb = (t3(kmax + 1) >> shift) + 1
+        assert tri.tet_lut_bytes(kmax, shift) == 8 * (kmax + 2) + 4 * (nb + 1)
+    for kmax, shift in [(0, 5), (2 ** 20, 5), (10, -1), (10, 41)]:
+        assert tri.tet_lut_bytes(kmax, shift) == 0
+    # validation happens before any launch (no GPU needed): NULL buffer, short buffer
+    assert L.tet_lut_build(511, 13, None, 0, None) == tri.TRI_EINVAL
+    assert L.tet_lut_build(511, 13, 8, tri.tet_lut_bytes(511, 13) - 1, None) == tri.TRI_EINVAL
+    assert L.tet_map_eval_lut(0, 10, 511, 13, None, None, 8, None) == tri.TRI_EINVAL

@@ -587,3 +587,47 @@ def test_collide1d_ranks_and_quantized(orc):
             sync()
             tot += cnt.item()
         assert tot == orc.collide1d(iv)
+
+
+# ============================================================== succinct LUT tetrahedral map
+@pytest.mark.parametrize("shift", [0, 4, 9, 40])
+def test_tet_lut_map_matches_enumeration(orc, shift):
+    """Layer index from the succinct table (S = T3, G = bucket starts) + 2-D lambda:
+    identical to the triple-loop enumeration, every Eq. / successor check passes."""
+    I, J, K = orc.enumerate_tet(120)
+    kmax, cnt = 119, len(I) - 1                 # omega + 1 is mapped too: stay below T3(120)
+    lut = torch.empty(tri.tet_lut_bytes(kmax, shift), dtype=torch.uint8, device="cuda")
+    tri.tet_lut_build(kmax, shift, lut)
+    ijk = torch.empty(3 * cnt, dtype=torch.int32, device="cuda")
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tet_map_eval_lut(0, cnt, kmax, shift, lut, ijk, fail)
+    sync()
+    got = ijk.cpu().numpy().astype(np.uint32).reshape(-1, 3)
+    assert np.array_equal(got[:, 0], I[:cnt]) and np.array_equal(got[:, 1], J[:cnt])
+    assert np.array_equal(got[:, 2], K[:cnt])
+    assert fail.item() == 0
+
+
+@pytest.mark.parametrize("kmax,shift,w0,count", [(511, 13, 0, None), (4000, 20, None, 1 << 24)])
+def test_tet_lut_map_equals_cbrt_map(kmax, shift, w0, count):
+    """n = 4096 at rho = 8 (512 layers, every omega) and a 4001-layer table near its end:
+    the table map and the cube-root map give the same (i, j, k)."""
+    end = (kmax + 1) * (kmax + 2) * (kmax + 3) // 6
+    if count is None:
+        count = end - 1
+    if w0 is None:
+        w0 = end - 1 - count
+    lut = torch.empty(tri.tet_lut_bytes(kmax, shift), dtype=torch.uint8, device="cuda")
+    tri.tet_lut_build(kmax, shift, lut)
+    a = torch.empty(3 * count, dtype=torch.int32, device="cuda")
+    b = torch.empty_like(a)
+    fa = torch.zeros(1, dtype=torch.int64, device="cuda")
+    fb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tet_map_eval_lut(w0, count, kmax, shift, lut, a, fa)
+    tri.tet_map_eval(w0, count, b, fb)
+    sync()
+    assert fa.item() == 0 and fb.item() == 0
+    assert torch.equal(a, b)
+    with pytest.raises(tri.TriError) as e:                 # omega + 1 past the table
+        tri.tet_map_eval_lut(end - 1, 1, kmax, shift, lut, None, fa)
+    assert e.value.code == tri.TRI_ERANGE
