@@ -92,3 +92,96 @@ def test_ca_halo_exchange_matches_oracle(orc, world, n, rho, k):
     assert np.array_equal(got, orc.ca_run(n, inputs.ca_state(n, 42), steps * k))
     assert cnt == world * (world + 1) // 2
     assert e == [float(sum(range(world)))] * 5
+
+
+# ---------------------------------------------------------------- allreduce paths
+# Collision and triplet ranks own plain contiguous omega ranges (tri_map_init /
+# tet_map_init with snap = 0) and sum their partials with all_reduce.  Each worker
+# computes its partial over exactly its tiles (host lambda / tetrahedral map from the
+# C ABI), so the reduced result equals the single-process oracle only if the
+# partition covers every tile once and the collective sums correctly.
+def _tile_worker(rank, world, port, kind, n, rho, q):
+    try:
+        _init(rank, world, port)
+        from paper_1609_01490_b200 import dist as tdist, inputs, tri
+        if kind == "collide":
+            # 11-bit-quantised spheres: every fp32 op of the predicate is exact, so an
+            # fp64 evaluation decides identically (the oracle pin in test_oracle_pins)
+            s = inputs.spheres_quantized(n, 7, 11, 0.1).astype(np.float64)
+            m = tri.tri_map_init(n, rho, 1, rank, world, 0)
+            cnt = 0
+            for w in range(m.omega_begin, m.omega_end):
+                bi, bj = tri.tri_lambda(w)
+                I = np.arange(bi * rho, min(n, bi * rho + rho))
+                J = np.arange(bj * rho, min(n, bj * rho + rho))
+                if len(I) == 0 or len(J) == 0:
+                    continue
+                d = s[I][:, None, :3] - s[J][None, :, :3]
+                d2 = (d * d).sum(-1)
+                rr = s[I][:, None, 3] + s[J][None, :, 3]
+                cnt += int(((d2 < rr * rr) & (J[None, :] < I[:, None])).sum())
+            c = torch.tensor([cnt], dtype=torch.int64)
+            tdist.allreduce_count(c)
+            res = int(c.item())
+        else:
+            p = inputs.points4(n, 42).astype(np.float64)
+            m = tri.tet_map_init(n, rho, rank, world)
+            e = np.zeros(n)
+            for w in range(m.omega_begin, m.omega_end):
+                ib, jb, kb = tri.tet_lambda(w)
+                for pp in range(kb * rho, min(n, kb * rho + rho)):
+                    for qq in range(ib * rho, min(n, ib * rho + rho)):
+                        if qq >= pp:
+                            continue
+                        S = np.arange(jb * rho, min(n, jb * rho + rho))
+                        S = S[S < qq]
+                        if len(S) == 0:
+                            continue
+                        a = ((p[pp, :3] - p[qq, :3]) ** 2).sum()
+                        b = ((p[qq, :3] - p[S, :3]) ** 2).sum(-1)
+                        c2 = ((p[S, :3] - p[pp, :3]) ** 2).sum(-1)
+                        abc = a * b * c2
+                        P = (a + c2 - b) * (a + b - c2) * (b + c2 - a)
+                        E = (1.0 + 3.0 * P / (8.0 * abc)) / abc ** 1.5
+                        e[pp] += E.sum() / 3
+                        e[qq] += E.sum() / 3
+                        np.add.at(e, S, E / 3)
+            et = torch.from_numpy(e)
+            tdist.allreduce_energy(et)
+            res = et.numpy().tolist()
+        if rank == 0:
+            q.put(res)
+        dist.destroy_process_group()
+    except Exception as ex:  # surface worker errors
+        q.put(repr(ex))
+        raise
+
+
+def _run_tiles(kind, world, n, rho):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tile_worker, args=(g, world, port, kind, n, rho, q)) for g in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert not isinstance(res, str), res
+    return res
+
+
+@pytest.mark.parametrize("world,n,rho", [(2, 600, 16), (3, 517, 32)])
+def test_collide_partition_allreduce_matches_oracle(orc, world, n, rho):
+    from paper_1609_01490_b200 import inputs
+    got = _run_tiles("collide", world, n, rho)
+    want = orc.collide(inputs.spheres_quantized(n, 7, 11, 0.1))
+    assert want > 100 and got == want
+
+
+@pytest.mark.parametrize("world,n,rho", [(2, 48, 4), (3, 61, 8)])
+def test_triplet_partition_allreduce_matches_oracle(orc, world, n, rho):
+    from paper_1609_01490_b200 import inputs
+    got = np.array(_run_tiles("triplet", world, n, rho))
+    want = orc.triplet(inputs.points4(n, 42))
+    assert np.allclose(got, want, rtol=1e-9, atol=1e-12 * np.abs(want).max())
