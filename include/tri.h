@@ -197,7 +197,7 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
                        const uint8_t *d_halo_below, void *d_ws, void *stream);
 
 /* k generations of the same rule in one call (temporal blocking, deep halos;
- * k in 1..8, rho = 128): d_out = the state after k generations of the whole
+ * k in 1..16, rho = 128): d_out = the state after k generations of the whole
  * domain restricted to this rank's slice, given the current state of the
  * rank's rows (d_in) and of the k rows on either side.  d_halo_above = the
  * packed rows [max(row_begin - k, 0), row_begin) (contiguous in the owner's

@@ -206,7 +206,7 @@ tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const
     (void)d_ws;
     if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
-    if (map->rho != 128 || k < 1 || k > 8) return TRI_EINVAL;
+    if (map->rho != 128 || k < 1 || k > 16) return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
     return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);

@@ -588,22 +588,7 @@ tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
 namespace multi {
 
 constexpr int RHO = 128;
-constexpr int KMAX = 8;
-constexpr int NINMAX = RHO + 2 * KMAX;   // input rows
-constexpr int NW = 5;                    // bitmap words per row: bit x <-> column c0 - k + x (rho + 2k <= 160)
-constexpr int RB = 4;                     // phase B: rows per band (register-resident)
-constexpr int BPW = 32 / NW;             // bands per warp (6: lanes 0..29, lanes 30, 31 idle in B)
-constexpr int NBAND = NINMAX / RB;       // 36 bands x 4 rows = the 144-row region
-constexpr int NT = 32 * ((NBAND + BPW - 1) / BPW);   // 192 threads
-static_assert(NBAND * RB == NINMAX, "bands tile the region");
-constexpr int RAWB = 32 * (NW + 1);      // loaded bytes per row (>= 15 + rho + 2k)
-constexpr int NCH = RAWB / 16;
-
-struct Smem {
-    uint32_t A[NINMAX][NW];                   // packed region (phase A) / final state (phase C)
-    uint32_t top[2][NBAND][NW], bot[2][NBAND][NW];   // band edge rows, double-buffered by generation
-    uint64_t seg[RHO];
-};
+constexpr int RB = 4;                    // phase B: rows per band (register-resident)
 
 template <bool B> struct MaskTag { static constexpr bool value = B; };
 
@@ -617,7 +602,30 @@ __device__ __forceinline__ uint32_t tri_mask(int64_t r, int64_t n, int64_t cb) {
     return up & ~((1u << lo) - 1u);
 }
 
-__device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
+// Geometry for NW bitmap words per row (bit x <-> column c0 - k + x): NW = 5 serves
+// k <= 8 (160 columns, 192 threads), NW = 6 serves k <= 16 (192 columns, 256 threads).
+template <int NWV>
+struct Multi {
+    static constexpr int NW = NWV;
+    static constexpr int KMAX = NW == 5 ? 8 : 16;
+    // garbage from the right edge reaches column c0 + 32 NW - 2K; phase C reads up to c0 + rho + 14
+    static_assert(32 * NW - 2 * KMAX >= RHO + 15, "bitmap too narrow for KMAX");
+    static constexpr int NINMAX = RHO + 2 * KMAX;          // region rows
+    static constexpr int BPW = 32 / NW;                    // bands per warp (lanes past BPW NW idle in B)
+    static constexpr int NBAND = NINMAX / RB;
+    static constexpr int NT = 32 * ((NBAND + BPW - 1) / BPW);
+    static_assert(NBAND * RB == NINMAX, "bands tile the region");
+    static_assert(NT >= NINMAX, "phase A: one thread per region row");
+    static constexpr int RAWB = 32 * (NW + 1);             // loaded bytes per row (>= 15 + rho + 2k)
+    static constexpr int NCH = RAWB / 16;
+
+    struct Smem {
+        uint32_t A[NINMAX][NW];                            // packed region (phase A) / final state (phase C)
+        uint32_t top[2][NBAND][NW], bot[2][NBAND][NW];     // band edge rows, double-buffered by generation
+        uint64_t seg[RHO];
+    };
+
+static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
     const int t = threadIdx.x;
     const int K = (int)a.k;
     const int NIN = RHO + 2 * K;
@@ -806,52 +814,62 @@ __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, 
     }
 }
 
-// 7 CTAs per SM (40 registers, a few spills) hide more of phase A's load latency
-// than 5 CTAs without spills: 0.270 -> 0.250 ms at K = 1, n = 32768.
-template <int STRAT>
-__global__ void __launch_bounds__(NT, 7) ca_multi_kernel(CaArgs a) {
-    __shared__ __align__(16) Smem sm;
+};
+
+// NW = 5: 7 CTAs per SM (40 registers, a few spills) hide more of phase A's load
+// latency than 5 CTAs without spills: 0.270 -> 0.250 ms at K = 1, n = 32768.
+template <int NWV, int STRAT>
+__global__ void __launch_bounds__(Multi<NWV>::NT, NWV == 5 ? 7 : 4) ca_multi_kernel(CaArgs a) {
+    using M = Multi<NWV>;
+    __shared__ __align__(16) typename M::Smem sm;
     if (STRAT == TRI_BB) {
         if (blockIdx.x > blockIdx.y + (uint32_t)a.tile_row_begin) return;
-        tile(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm);
+        M::tile(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm);
     } else if (STRAT == TRI_LAMBDA) {
         const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
         if (w >= a.omega_end) return;
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
-        tile(a, bi, bj, sm);
+        M::tile(a, bi, bj, sm);
     } else {
 #pragma unroll 1
         for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
-            tile(a, t.bi, t.bj, sm);
+            M::tile(a, t.bi, t.bj, sm);
             __syncthreads();                                  // smem reused by the next tile
         }
     }
 }
 
-tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+template <int NWV>
+tri_status launch_nw(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+    constexpr int NT = Multi<NWV>::NT;
     if (strategy == TRI_BB) {
         const int64_t tr0 = m.row_begin / m.rho;
         const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;
         if (tr1 <= tr0) return TRI_OK;
         if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
         a.tile_row_begin = tr0;
-        ca_multi_kernel<TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
+        ca_multi_kernel<NWV, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
     } else if (strategy == TRI_LAMBDA) {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
-        ca_multi_kernel<TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
+        ca_multi_kernel<NWV, TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
     } else {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<TRI_LAMBDA_PERSIST>, NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<NWV, TRI_LAMBDA_PERSIST>, NT, 0);
         uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
         if (g > nb) g = nb;
-        ca_multi_kernel<TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
+        ca_multi_kernel<NWV, TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
     }
     tri::note_launches(1);
     return tri::cuda_status();
+}
+
+
+tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+    return a.k <= Multi<5>::KMAX ? launch_nw<5>(m, strategy, a, st) : launch_nw<6>(m, strategy, a, st);
 }
 
 }  // namespace multi

@@ -389,39 +389,41 @@ def ca_steps_gpu(n, state, calls, k, strategy, world=1, fill=None):
 
 
 @pytest.mark.parametrize("strategy", STRATS)
-@pytest.mark.parametrize("k", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 9, 12, 16])
 @pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (17, 7), (130, 42), (1000, 7), (2049, 42)])
 def test_ca_steps_single(orc, strategy, k, n, seed):
     st = inputs.ca_state(n, seed)
     assert np.array_equal(ca_steps_gpu(n, st, 2, k, strategy), orc.ca_run(n, st, 2 * k))
 
 
-@pytest.mark.parametrize("world,k", [(2, 4), (3, 3), (4, 8), (3, 1)])
+@pytest.mark.parametrize("world,k", [(2, 4), (3, 3), (4, 8), (3, 1), (2, 16), (3, 11)])
 def test_ca_steps_deep_halo_ranks(orc, world, k):
     n = 2000
     st = inputs.ca_state(n, 42)
     assert np.array_equal(ca_steps_gpu(n, st, 3, k, "lambda", world), orc.ca_run(n, st, 3 * k))
 
 
-@pytest.mark.parametrize("k", [1, 4])
+@pytest.mark.parametrize("k", [1, 4, 16])
 def test_ca_steps_ignores_garbage(orc, k):
     n = 2049
     st = inputs.ca_state(n, 7)
     assert np.array_equal(ca_steps_gpu(n, st, 2, k, "lambda", 1, fill=255), orc.ca_run(n, st, 2 * k))
 
 
-def test_ca_steps_full_size_sampled(orc):
-    """BASELINE configs[3] (n = 32768) with the bench's k = 4 launch, sampled rows."""
+@pytest.mark.parametrize("k", [4, 8, 16])
+def test_ca_steps_full_size_sampled(orc, k):
+    """BASELINE configs[3] (n = 32768) with k-generation launches (the bench's plan uses
+    the k it measures fastest), sampled rows."""
     n = 32768
     st = inputs.ca_state(n, 42)
     m = tri.tri_map_init(n, 128)
     a = torch.from_numpy(st).cuda()
     b = torch.empty_like(a)
-    tri.tri_ca_steps(m, "lambda", 4, a, b)
+    tri.tri_ca_steps(m, "lambda", k, a, b)
     sync()
     got = b.cpu().numpy()
     ref = st
-    for _ in range(4):
+    for _ in range(k):
         ref = orc.ca_step(n, ref)
     for rb, re in [(0, 40), (16380, 16390), (32700, 32768)]:
         assert np.array_equal(got[T(rb):T(re)], ref[T(rb):T(re)])
