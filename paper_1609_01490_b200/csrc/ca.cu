@@ -1,7 +1,11 @@
-// ca.cu -- one generation of Life B3/S23 on the triangular domain
-// {(i, j): 0 <= j <= i < n} (P:79-80 names cellular automata on triangular
-// domains, citing Conway's Life; cells outside the triangle are dead --
-// DESIGN.md reading Q11).  State: u8 {0,1} in the packed Eq. 1 layout.
+// ca.cu -- Life B3/S23 on the triangular domain {(i, j): 0 <= j <= i < n}
+// (P:79-80 names cellular automata on triangular domains, citing Conway's
+// Life; cells outside the triangle are dead -- DESIGN.md reading Q11).
+// State: u8 {0,1} in the packed Eq. 1 layout.  Three kernels:
+//   rho = 128: multi::ca_multi_kernel -- k generations per launch on a
+//              register-resident bitmap (tri_ca_steps; tri_ca_step is k = 1);
+//   rho = 256: bits::ca_bits_kernel -- one generation, shared-memory bitmaps;
+//   rho = 512: ca_kernel -- one generation, byte SWAR (described next).
 //
 // Block-space mapping: a rho x rho tile from lambda(omega) or the
 // BB grid; inside the tile, every aligned 16-byte CHUNK of the output slice is
