@@ -238,13 +238,14 @@ tri_status launch_r(const tet_map_t &m, int strategy, TripArgs a, cudaStream_t s
 //     equal (k, i)),
 //   * e_s is a 32-value register vector reduce-scattered across the warp once
 //     per tile (~0.12 shuffles per triplet).
-// Three squared-distance tables per warp live in shared memory, padded so every
-// access pattern is conflict-free: Dpq[p][q] (stride 33, per-lane scalar),
-// Dps[p][s] (stride 36, per-lane LDS.128), Dqs[q][s] (stride 32, broadcast
-// LDS.128).  Two s values are processed per instruction with the packed
-// sm_100 f32x2 ops; MUFU.RSQ stays scalar.
-//   E = r^3 + 0.375 P r^5 with r = (abc)^-1/2, P = (b+c-a)(a-b+c)(a+b-c),
-// computed as u' = 0.375 (b + c) - 0.375 a (one FFMA), v = a - (b - c), w = a + (b - c).
+// Two squared-distance tables per warp live in shared memory, padded so every
+// access pattern is conflict-free: Dps[p][s] (stride 36, per-lane LDS.128) and
+// Dqs[q][s] (stride 32, broadcast LDS.128); a = |x_p - x_q|^2 is recomputed per
+// q (5 ops per 32 triplets -- cheaper than the 4 KB table it replaces, which
+// bought occupancy: 5.52 -> 5.35 ms).  Two s values are processed per
+// instruction with the packed sm_100 f32x2 ops; MUFU.RSQ stays scalar.
+//   E = r^3 (1 + P' r^2), r = (abc)^-1/2, P' = 3/8 (b+c-a)(a-b+c)(a+b-c)
+// (see atm2 for the operation order).
 namespace t32 {
 
 typedef unsigned long long f2;
@@ -295,7 +296,6 @@ struct WarpSmem {
     float4 P[32], Q[32], S[32];
     float Dqs[32][32];
     float Dps[32][36];
-    float Dpq[32][33];
 };
 
 __device__ __forceinline__ float d2f(const float4 a, const float4 b) {
@@ -340,13 +340,10 @@ __device__ __forceinline__ void tile(const TripArgs &a, WarpSmem &sm, uint32_t k
         sm.Dqs[r][lane] = d2f(sm.Q[r], myS);
         sm.Dps[r][lane] = d2f(sm.P[r], myS);
     }
-    if (new_pq) {
-        const float4 myQ = sm.Q[lane];
-#pragma unroll 4
-        for (int r = 0; r < 32; ++r) sm.Dpq[r][lane] = d2f(sm.P[r], myQ);
-    }
+
     __syncwarp();
     const int64_t p = (int64_t)kb * 32 + lane;
+    const float4 myP = sm.P[lane];
     const f2 nc375 = pk(-0.375f, -0.375f), one = pk(1.f, 1.f);
     f2 es[16];
 #pragma unroll
@@ -354,7 +351,7 @@ __device__ __forceinline__ void tile(const TripArgs &a, WarpSmem &sm, uint32_t k
     float accp = 0.f, myq = 0.f;
 #pragma unroll 1
     for (int q = 0; q < 32; ++q) {
-        const float av = sm.Dpq[lane][q];
+        const float av = d2f(myP, sm.Q[q]);                 // a = |x_p - x_q|^2, recomputed per q
         const f2 aa = pk(av, av), a375 = pk(0.375f * av, 0.375f * av), na2 = pk(-av * av, -av * av);
         f2 row = 0ull, row2 = 0ull;
         bool pq_ok = true;
@@ -442,10 +439,10 @@ __device__ __forceinline__ void run_tile(const TripArgs &a, WarpSmem &sm, uint32
         tile<false>(a, sm, kb, ib, jb, new_pq, acc);
 }
 
-constexpr int kWarps = 2;          // 2 x 14.4 KB of tables per CTA (static smem limit 48 KB)
+constexpr int kWarps = 2;          // 2 x 10 KB of tables per CTA
 
 template <int STRAT>
-__global__ void __launch_bounds__(32 * kWarps, 8) triplet32_kernel(TripArgs a) {
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps) triplet32_kernel(TripArgs a) {
     __shared__ __align__(16) WarpSmem smem[kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem &sm = smem[warp];
