@@ -694,10 +694,10 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
     // shared memory (one exchange per generation).  What enters at the region
     // edges (the shuffle partners of words 0 and NW-1, rows past the staged
     // region, idle lanes) is garbage that moves one cell per generation: after K
-    // generations it reaches column c0 - 1 on the left, c0 + 160 - 2K >= c0 + 144
-    // on the right and rows outside [K, K + rho) -- never a cell phase C writes.
+    // generations it reaches column c0 - 1 on the left, c0 + 32 NW - 2K >= c0 + rho
+    // + 15 on the right and rows outside [K, K + rho) -- never a cell phase C writes.
     // Cells outside the triangle are re-masked dead every generation (skipped
-    // when the whole warp's mask is all ones).
+    // when the whole CTA's mask is all ones).
     {
         const int lane = t & 31;
         const bool act = lane < BPW * NW;
@@ -717,7 +717,8 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
             Mk[q] = (in && !inside) ? tri_mask(r0 - K + y, a.n, cs + 32 * w) : 0xffffffffu;
             ones = ones && Mk[q] == 0xffffffffu;
         }
-        const bool nomask = inside || __all_sync(0xffffffffu, ones);
+        // block-uniform (the generation loops below contain __syncthreads)
+        const bool nomask = __syncthreads_and(inside || ones) != 0;
         auto hsum = [&](uint32_t V, uint32_t &s0, uint32_t &s1, uint32_t &q0, uint32_t &q1) {
             const uint32_t Vp = __shfl_up_sync(0xffffffffu, V, 1);
             const uint32_t Vn = __shfl_down_sync(0xffffffffu, V, 1);
