@@ -335,25 +335,29 @@ def bench_collide(rank, world, pk):
 def bench_ca(rank, world, pk, steps=100):
     import torch
     from paper_1609_01490_b200 import dist as tdist, inputs, tri
-    n, rho = 32768, 128
-    st = inputs.ca_state(n, 42)
-    maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
-    m = maps[rank]
-    bounds = [(x.row_begin, x.row_end) for x in maps]
-    full = torch.from_numpy(st)
-    a = full[m.out_offset:m.out_offset + m.out_cells].clone().cuda()
-    b = torch.empty_like(a)
-    res = {}
-    bufs = [a, b]
+    n = 32768
+    RHO1, RHOK = 128, 224          # tile edges: tri_ca_step (k = 1) and tri_ca_steps (the faster geometry for each)
     K = 8                                              # generations per tri_ca_steps launch (deep halos)
+    st = inputs.ca_state(n, 42)
+    full = torch.from_numpy(st)
     plan = [K] * (steps // K) + ([steps % K] if steps % K else [])
-    halo = {}
-    for k in set(plan) | {1}:
-        na, nb = tdist.halo_bytes(bounds, n, rank, k)
-        halo[k] = (torch.zeros(max(na, 1), dtype=torch.uint8, device="cuda") if m.row_begin > 0 else None,
-                   torch.zeros(max(nb, 1), dtype=torch.uint8, device="cuda") if m.row_end < n else None)
 
+    def setup(rho, ks):
+        maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+        m = maps[rank]
+        bounds = [(x.row_begin, x.row_end) for x in maps]
+        a = full[m.out_offset:m.out_offset + m.out_cells].clone().cuda()
+        halo = {}
+        for k in ks:
+            na, nb = tdist.halo_bytes(bounds, n, rank, k)
+            halo[k] = (torch.zeros(max(na, 1), dtype=torch.uint8, device="cuda") if m.row_begin > 0 else None,
+                       torch.zeros(max(nb, 1), dtype=torch.uint8, device="cuda") if m.row_end < n else None)
+        return m, bounds, [a, torch.empty_like(a)], halo
+
+    res = {}
     # single-generation kernel (tri_ca_step, one halo row each side every step)
+    m, bounds, bufs, halo = setup(RHO1, {1})
+    cells1 = m.out_cells
     for strat in ("bb", "persist", "lambda"):
         def run(strat=strat):
             x, y = bufs
@@ -366,6 +370,7 @@ def bench_ca(rank, world, pk, steps=100):
         t, _ = time_steps(run, 1, 1, world)
         res["step_" + strat + "_ms"] = round(max_over_ranks(t, world), 3)
     # K generations per launch (tri_ca_steps, K-row halos every K steps)
+    m, bounds, bufs, halo = setup(RHOK, set(plan))
     for strat in ("bb", "lambda"):
         def run(strat=strat):
             x, y = bufs
@@ -377,6 +382,7 @@ def bench_ca(rank, world, pk, steps=100):
                 x, y = y, x
         t, _ = time_steps(run, 1, 1, world)
         res[strat + "_ms"] = round(max_over_ranks(t, world), 3)
+    res["rho_single_step"], res["rho_k_steps"] = RHO1, RHOK
     best = res["lambda_ms"]
     res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
     res["I_lambda_single_step"] = round(res["step_bb_ms"] / res["step_lambda_ms"], 4)
@@ -385,7 +391,7 @@ def bench_ca(rank, world, pk, steps=100):
     # per launch the kernel reads + writes each cell once: 2 B/cell per K generations
     launches = len(plan)
     gbs = 2 * (m.out_cells * launches) / (best * 1e-3) / 1e9
-    gbs1 = 2 * (m.out_cells * steps) / (res["step_lambda_ms"] * 1e-3) / 1e9
+    gbs1 = 2 * (cells1 * steps) / (res["step_lambda_ms"] * 1e-3) / 1e9
     res["roofline"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                        "frac": round(gbs / pk["hbm_gbs"], 4), "bytes_per_cell_generation": round(2 / K, 3),
                        "note": f"tri_ca_steps, {K} generations per launch; the single-step kernel reaches "

@@ -191,13 +191,13 @@ size_t tri_ca_workspace_size(const tri_map_t *map);
  * packed slice (out_cells bytes, u8 {0,1}, 16-byte aligned, must not alias).
  * d_halo_above = row row_begin-1 (row_begin bytes) or NULL (dead); d_halo_below
  * = row row_end (row_end+1 bytes) or NULL (dead; ignored when row_end == n).
- * rho (tile edge) in {128, 256, 512}.  d_ws: tri_ca_workspace_size bytes (NULL if 0). */
+ * rho (tile edge) in {128, 224, 256, 512}.  d_ws: tri_ca_workspace_size bytes (NULL if 0). */
 tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_in,
                        uint8_t *d_out, const uint8_t *d_halo_above,
                        const uint8_t *d_halo_below, void *d_ws, void *stream);
 
 /* k generations of the same rule in one call (temporal blocking, deep halos;
- * k in 1..16, rho = 128): d_out = the state after k generations of the whole
+ * k in 1..16 at rho = 128, 1..8 at rho = 224): d_out = the state after k generations of the whole
  * domain restricted to this rank's slice, given the current state of the
  * rank's rows (d_in) and of the k rows on either side.  d_halo_above = the
  * packed rows [max(row_begin - k, 0), row_begin) (contiguous in the owner's

@@ -194,7 +194,7 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
     (void)d_ws;
     if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
-    if (map->rho != 128 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
+    if (map->rho != 128 && map->rho != 224 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
     return launch_ca(*map, strategy, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);
@@ -206,7 +206,7 @@ tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const
     (void)d_ws;
     if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
-    if (map->rho != 128 || k < 1 || k > 16) return TRI_EINVAL;
+    if (k < 1 || !((map->rho == 128 && k <= 16) || (map->rho == 224 && k <= 8))) return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
     return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);

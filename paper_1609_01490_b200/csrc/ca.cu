@@ -375,6 +375,25 @@ __device__ __forceinline__ uint32_t pack32(const uint4 lo, const uint4 hi) {
 // 4 bits -> 4 bytes {0,1}: nibble * 0x00204081 puts bit q at 8q (no collisions).
 __device__ __forceinline__ uint32_t spread4(uint32_t v) { return (v * 0x00204081u) & 0x01010101u; }
 
+// One LOP3 with truth table F over (a, b, c) = (0xf0, 0xcc, 0xaa).
+template <int F>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(F));
+    return d;
+}
+// Integer multiply-adds (FMA pipe): lo(a b) + c and hi(a b) + c.
+__device__ __forceinline__ uint32_t imad_lo(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t imad_hi(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 template <int RHO>
 struct Smem {
     uint32_t in[Cfg<RHO>::NIN][Cfg<RHO>::NW];
@@ -591,7 +610,6 @@ tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
 // 2 bytes to about (1.2 + 1) / k bytes.
 namespace multi {
 
-constexpr int RHO = 128;
 constexpr int RB = 4;                    // phase B: rows per band (register-resident)
 
 template <bool B> struct MaskTag { static constexpr bool value = B; };
@@ -606,25 +624,42 @@ __device__ __forceinline__ uint32_t tri_mask(int64_t r, int64_t n, int64_t cb) {
     return up & ~((1u << lo) - 1u);
 }
 
-// Geometry for NW bitmap words per row (bit x <-> column c0 - k + x): NW = 5 serves
-// k <= 8 (160 columns, 192 threads), NW = 6 serves k <= 16 (192 columns, 256 threads).
-template <int NWV>
+// Geometry: rho x rho tiles, NW bitmap words per region row (bit x <-> column
+// c0 - k + x), WPT horizontally adjacent words per phase-B thread, k <= KMAX.
+//   <128, 5, 1,  8>: 160 columns, 192 threads (rho = 128, k <= 8)
+//   <128, 6, 1, 16>: 192 columns, 256 threads (rho = 128, k <= 16)
+//   <224, 8, 2,  8>: 256 columns, 256 threads (rho = 224, k <= 8): the region
+//       overhead (32 NW)(rho + 2k) / rho^2 falls from 1.41 to 1.22 at k = 8, no
+//       phase-B lane idles (4 threads per band, 8 bands per warp), and the word
+//       pair a thread owns halves the shuffles per cell (the inner neighbour bits
+//       come from the thread's own other word).
+template <int RHO_, int NWV, int WPT_, int KMAX_>
 struct Multi {
+    static constexpr int RHO = RHO_;
     static constexpr int NW = NWV;
-    static constexpr int KMAX = NW == 5 ? 8 : 16;
+    static constexpr int WPT = WPT_;
+    static constexpr int KMAX = KMAX_;
     // garbage from the right edge reaches column c0 + 32 NW - 2K; phase C reads up to c0 + rho + 14
     static_assert(32 * NW - 2 * KMAX >= RHO + 15, "bitmap too narrow for KMAX");
+    static_assert(NW % WPT == 0 && RHO % 16 == 0, "geometry");
     static constexpr int NINMAX = RHO + 2 * KMAX;          // region rows
-    static constexpr int BPW = 32 / NW;                    // bands per warp (lanes past BPW NW idle in B)
+    static constexpr int TPB = NW / WPT;                   // threads per band
+    static constexpr int BPW = 32 / TPB;                   // bands per warp (lanes past BPW TPB idle in B)
     static constexpr int NBAND = NINMAX / RB;
     static constexpr int NT = 32 * ((NBAND + BPW - 1) / BPW);
     static_assert(NBAND * RB == NINMAX, "bands tile the region");
     static_assert(NT >= NINMAX, "phase A: one thread per region row");
     static constexpr int RAWB = 32 * (NW + 1);             // loaded bytes per row (>= 15 + rho + 2k)
     static constexpr int NCH = RAWB / 16;
+    // phase C: LPR lanes per row, CPL consecutive 16-byte chunks per lane (two
+    // chunks per lane measured faster at rho = 224, slower at rho = 128 / k = 1)
+    static constexpr int LPR = 8;
+    static constexpr int CPL = RHO <= 128 ? 1 : 2;
+    static_assert(16 * CPL * LPR >= RHO && NT % LPR == 0, "phase C slots");
 
+    static constexpr int AW = NW | 1;                      // odd row stride: phase A's row-per-lane stores conflict-free
     struct Smem {
-        uint32_t A[NINMAX][NW];                            // packed region (phase A) / final state (phase C)
+        uint32_t A[NINMAX][AW];                            // packed region (phase A) / final state (phase C)
         uint32_t top[2][NBAND][NW], bot[2][NBAND][NW];     // band edge rows, double-buffered by generation
         uint64_t seg[RHO];
     };
@@ -700,11 +735,11 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
     // when the whole CTA's mask is all ones).
     {
         const int lane = t & 31;
-        const bool act = lane < BPW * NW;
-        const int w = act ? lane % NW : 0;
-        const int band = (t >> 5) * BPW + (act ? lane / NW : 0);
+        const bool act = lane < BPW * TPB;
+        const int w0 = act ? (lane % TPB) * WPT : 0;         // first owned word
+        const int band = (t >> 5) * BPW + (act ? lane / TPB : 0);
         const bool live = act && band < NBAND;
-        uint32_t X[RB], Mk[RB];
+        uint32_t X[RB][WPT], Mk[RB][WPT];
         // CTA-uniform: every region cell (rows r0-K .. r0+rho+K-1, bitmap columns
         // cs .. cs+32 NW-1) inside the triangle and the domain -> no masks at all
         const bool inside = cs >= 0 && cs + 32 * NW - 1 <= r0 - K && r0 + RHO + K <= a.n;
@@ -713,48 +748,82 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
         for (int q = 0; q < RB; ++q) {
             const int y = RB * band + q;
             const bool in = live && y < NIN;
-            X[q] = in ? sm.A[y][w] : 0u;
-            Mk[q] = (in && !inside) ? tri_mask(r0 - K + y, a.n, cs + 32 * w) : 0xffffffffu;
-            ones = ones && Mk[q] == 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < WPT; ++u) {
+                X[q][u] = in ? sm.A[y][w0 + u] : 0u;
+                Mk[q][u] = (in && !inside) ? tri_mask(r0 - K + y, a.n, cs + 32 * (w0 + u)) : 0xffffffffu;
+                ones = ones && Mk[q][u] == 0xffffffffu;
+            }
         }
         // block-uniform (the generation loops below contain __syncthreads)
         const bool nomask = __syncthreads_and(inside || ones) != 0;
-        auto hsum = [&](uint32_t V, uint32_t &s0, uint32_t &s1, uint32_t &q0, uint32_t &q1) {
-            const uint32_t Vp = __shfl_up_sync(0xffffffffu, V, 1);
-            const uint32_t Vn = __shfl_down_sync(0xffffffffu, V, 1);
-            const uint32_t L = __funnelshift_l(Vp, V, 1), R = __funnelshift_r(V, Vn, 1);
-            s0 = L ^ V ^ R;                                   // 3-cell row sum (bit 0, bit 1)
-            s1 = (L & V) | (L & R) | (V & R);
-            q0 = L ^ R;                                       // 2-cell sum without the centre
-            q1 = L & R;
+        // The ALU pipe (LOP3 / SHF) and the shuffle path are the limiters of phase B;
+        // the FMA pipe runs at the ALU's rate beside it, so the one-bit neighbour
+        // shifts go there as integer multiply-adds (L = 2V + (left >> 31),
+        // R = hi(V 2^31) + (right << 31)), and the logic is written as explicit
+        // 3-input LOP3s (the compiler's own factoring took 61 instead of 44 per
+        // 4 x 32 cells).  The multipliers 2 and 2^31 are hidden from the compiler
+        // (it would turn the multiply-adds back into ALU-pipe LEA.HI / SHF); a.n < 2^62.
+        const uint32_t two = 2u | (uint32_t)((uint64_t)a.n >> 62);
+        const uint32_t half = two << 30;
+        // row sums of one region row: s = L + V + R (bits s0, s1), p = L + R (p0, p1)
+        auto hsum = [&](const uint32_t (&V)[WPT], uint32_t (&s0)[WPT], uint32_t (&s1)[WPT], uint32_t (&q0)[WPT],
+                        uint32_t (&q1)[WPT], bool need_q) {
+            const uint32_t Vp = __shfl_up_sync(0xffffffffu, V[WPT - 1], 1);   // left thread's last word
+            const uint32_t Vn = __shfl_down_sync(0xffffffffu, V[0], 1);       // right thread's first word
+#pragma unroll
+            for (int u = 0; u < WPT; ++u) {
+                const uint32_t lw = u == 0 ? Vp : V[u - 1], rw = u == WPT - 1 ? Vn : V[u + 1];
+                const uint32_t L = bits::imad_lo(V[u], two, bits::imad_hi(lw, two, 0u));
+                const uint32_t R = bits::imad_hi(V[u], half, bits::imad_lo(rw, half, 0u));
+                s0[u] = bits::lop3<0x96>(L, V[u], R);
+                s1[u] = bits::lop3<0xe8>(L, V[u], R);
+                if (need_q) {
+                    q0[u] = L ^ R;
+                    q1[u] = L & R;
+                }
+            }
         };
         auto generations = [&](auto masked) {
 #pragma unroll 1
             for (int g = 0; g < K; ++g) {
                 const int pb = g & 1;
                 if (live) {
-                    sm.top[pb][band][w] = X[0];
-                    sm.bot[pb][band][w] = X[RB - 1];
+#pragma unroll
+                    for (int u = 0; u < WPT; ++u) {
+                        sm.top[pb][band][w0 + u] = X[0][u];
+                        sm.bot[pb][band][w0 + u] = X[RB - 1][u];
+                    }
                 }
                 __syncthreads();
-                const uint32_t up = (live && band > 0) ? sm.bot[pb][band - 1][w] : 0u;
-                const uint32_t dn = (live && band + 1 < NBAND) ? sm.top[pb][band + 1][w] : 0u;
-                uint32_t h0[RB + 2], h1[RB + 2], p0[RB], p1[RB], u0, u1;
-                hsum(up, h0[0], h1[0], u0, u1);
+                uint32_t up[WPT], dn[WPT];
 #pragma unroll
-                for (int q = 0; q < RB; ++q) hsum(X[q], h0[q + 1], h1[q + 1], p0[q], p1[q]);
-                hsum(dn, h0[RB + 1], h1[RB + 1], u0, u1);
+                for (int u = 0; u < WPT; ++u) {
+                    up[u] = (live && band > 0) ? sm.bot[pb][band - 1][w0 + u] : 0u;
+                    dn[u] = (live && band + 1 < NBAND) ? sm.top[pb][band + 1][w0 + u] : 0u;
+                }
+                uint32_t h0[RB + 2][WPT], h1[RB + 2][WPT], p0[RB][WPT], p1[RB][WPT], u0[WPT], u1[WPT];
+                hsum(up, h0[0], h1[0], u0, u1, false);
+#pragma unroll
+                for (int q = 0; q < RB; ++q) hsum(X[q], h0[q + 1], h1[q + 1], p0[q], p1[q], true);
+                hsum(dn, h0[RB + 1], h1[RB + 1], u0, u1, false);
 #pragma unroll
                 for (int q = 0; q < RB; ++q) {
-                    // neighbour count = h(row above) + h(row below) + p(own row), bit-sliced
-                    const uint32_t a0 = h0[q], b0 = h0[q + 2], c0_ = p0[q];
-                    const uint32_t a1 = h1[q], b1 = h1[q + 2], c1 = p1[q];
-                    const uint32_t z0 = a0 ^ b0 ^ c0_;
-                    const uint32_t k0 = (a0 & b0) | (a0 & c0_) | (b0 & c0_);
-                    const uint32_t x = a1 ^ b1 ^ c1;
-                    const uint32_t ge2 = (a1 & b1) | (a1 & c1) | (b1 & c1);
-                    const uint32_t nx = (~ge2 & (x ^ k0)) & (z0 | X[q]);
-                    X[q] = decltype(masked)::value ? nx & Mk[q] : nx;
+#pragma unroll
+                    for (int u = 0; u < WPT; ++u) {
+                        // neighbour count = h(row above) + h(row below) + p(own row), bit-sliced:
+                        // count = z0 + 2 (x + k0) + 4 ge2; alive' <=> count == 3, or count == 2
+                        // and alive <=> (x + k0 + 2 ge2 == 1) and (z0 | alive)
+                        const uint32_t a0 = h0[q][u], b0 = h0[q + 2][u], c0_ = p0[q][u];
+                        const uint32_t a1 = h1[q][u], b1 = h1[q + 2][u], c1 = p1[q][u];
+                        const uint32_t z0 = bits::lop3<0x96>(a0, b0, c0_);
+                        const uint32_t k0 = bits::lop3<0xe8>(a0, b0, c0_);
+                        const uint32_t x = bits::lop3<0x96>(a1, b1, c1);
+                        const uint32_t ge2 = bits::lop3<0xe8>(a1, b1, c1);
+                        const uint32_t one = bits::lop3<0x06>(ge2, x, k0);      // ~ge2 & (x ^ k0)
+                        const uint32_t nx = bits::lop3<0xe0>(one, z0, X[q][u]); // one & (z0 | X)
+                        X[q][u] = decltype(masked)::value ? nx & Mk[q][u] : nx;
+                    }
                 }
             }
         };
@@ -764,28 +833,34 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
             const int y = RB * band + q;
-            if (live && y < NINMAX) sm.A[y][w] = X[q];
+#pragma unroll
+            for (int u = 0; u < WPT; ++u)
+                if (live && y < NINMAX) sm.A[y][w0 + u] = X[q][u];
         }
         __syncthreads();
     }
-    uint32_t (*fin)[NW] = sm.A;
+    uint32_t (*fin)[AW] = sm.A;
     // ---- C: aligned-chunk ownership (a 16-byte chunk is written by the tile
     // holding its first cell; the region covers the <= 15-column spill past the
-    // tile for K <= 8).  Byte stores only where a chunk crosses a row boundary:
+    // tile for K <= KMAX).  Byte stores only where a chunk crosses a row boundary:
     // the row-i part of a chunk running past the row end (diagonal tiles), and
     // the head bytes of a row whose first chunk started in the previous row (c0 = 0).
-    // A warp covers 4 rows x 8 chunk slots per pass (lane = 8 row + slot), so
-    // each warp store is four 128-byte runs.  A row segment of len <= rho cells
-    // starting at phase delta touches slots 0..7 only.
-    const int slot = t & 7;
+    // LPR lanes per row, CPL consecutive chunks per lane (one 32-bit window of the
+    // bitmap), 32 / LPR rows per warp pass.  A row segment of len <= rho cells
+    // starting at phase delta has chunks at delta + 16 c < len, c < rho / 16.
+    const int slot = t & (LPR - 1);
     // owned tile rows [rr_lo, rr_hi) and the row offset r0 - c0, in 32 bits
     const int64_t lo64 = a.R0 - r0, hi64 = a.R1 - r0;
     const int rr_lo = lo64 < 0 ? 0 : (lo64 > RHO ? RHO : (int)lo64);
     const int rr_hi = hi64 < 0 ? 0 : (hi64 > RHO ? RHO : (int)hi64);
     const int64_t dr64 = r0 - c0 + 1;                         // seg(rr) = dr + rr cells in the row from c0
     const int dr = dr64 > (1 << 20) ? (1 << 20) : (dr64 < -RHO ? -RHO : (int)dr64);
+    auto chunk = [](uint32_t h) {                             // 16 bits -> 16 bytes {0,1}
+        return make_uint4(bits::spread4(h & 15u), bits::spread4((h >> 4) & 15u), bits::spread4((h >> 8) & 15u),
+                          bits::spread4((h >> 12) & 15u));
+    };
 #pragma unroll 1
-    for (int rr = (t >> 3) + rr_lo; rr < rr_hi; rr += NT / 8) {
+    for (int rr = t / LPR + rr_lo; rr < rr_hi; rr += NT / LPR) {
         const int seg = dr + rr;
         if (seg <= 0) continue;
         const int len = seg < RHO ? seg : RHO;
@@ -800,20 +875,31 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
                 a.out[s + u] = (uint8_t)((fin[y][x >> 5] >> (x & 31)) & 1u);
             }
         }
-        const int off = delta + 16 * slot;
+        const int off = delta + 16 * CPL * slot;              // chunks [off, off + 16) (and [off + 16, off + 32))
         if (off >= len) continue;
-        const int x = off + K;
-        if (off + 16 <= seg) {
-            const uint32_t w0 = fin[y][x >> 5];
-            const uint32_t w1 = (x >> 5) + 1 < NW ? fin[y][(x >> 5) + 1] : 0u;
-            const uint32_t b = __funnelshift_r(w0, w1, (uint32_t)(x & 31));
-            st_cs_v4u(a.out + s + off, bits::spread4(b & 15u), bits::spread4((b >> 4) & 15u),
-                      bits::spread4((b >> 8) & 15u), bits::spread4((b >> 12) & 15u));
-        } else {                                               // crosses the row end: row-i part only
+        const int x = off + K, wi = x >> 5;
+        const uint32_t w0 = fin[y][wi];
+        const uint32_t w1 = wi + 1 < NW ? fin[y][wi + 1] : 0u;
+        const uint32_t b = __funnelshift_r(w0, w1, (uint32_t)(x & 31));   // cells off .. off + 31
+        uint8_t *dst = a.out + s + off;
+        const bool second = CPL == 2 && off + 16 < len;       // a second chunk, and it is this tile's
+        if (CPL == 2 && second && off + 32 <= seg) {
+            const uint4 v0 = chunk(b), v1 = chunk(b >> 16);
+            st_cs_v4u(dst, v0.x, v0.y, v0.z, v0.w);
+            st_cs_v4u(dst + 16, v1.x, v1.y, v1.z, v1.w);
+        } else {
+            // a chunk crossing the row end: its row-i part only (if the second chunk
+            // exists and crosses, the first is full)
+            const int end = seg - off < 32 ? seg - off : 32;
+            int u = 0;
+            if (off + 16 <= seg) {
+                const uint4 v0 = chunk(b);
+                st_cs_v4u(dst, v0.x, v0.y, v0.z, v0.w);
+                u = 16;
+            }
+            if (u == 0 || second) {
 #pragma unroll 1
-            for (int u = 0; u < seg - off; ++u) {
-                const int xu = x + u;
-                a.out[s + off + u] = (uint8_t)((fin[y][xu >> 5] >> (xu & 31)) & 1u);
+                for (; u < end; ++u) dst[u] = (uint8_t)((b >> u) & 1u);
             }
         }
     }
@@ -821,11 +907,16 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
 
 };
 
-// NW = 5: 7 CTAs per SM (40 registers, a few spills) hide more of phase A's load
+using G5 = Multi<128, 5, 1, 8>;     // rho = 128, k <= 8
+using G6 = Multi<128, 6, 1, 16>;    // rho = 128, 9 <= k <= 16
+using G8 = Multi<224, 8, 2, 8>;     // rho = 224, k <= 8
+
+// G5: 7 CTAs per SM (40 registers, a few spills) hide more of phase A's load
 // latency than 5 CTAs without spills: 0.270 -> 0.250 ms at K = 1, n = 32768.
-template <int NWV, int STRAT>
-__global__ void __launch_bounds__(Multi<NWV>::NT, NWV == 5 ? 7 : 4) ca_multi_kernel(CaArgs a) {
-    using M = Multi<NWV>;
+template <class M> constexpr int min_ctas() { return M::NW == 5 ? 7 : (M::NW == 6 ? 4 : 4); }
+
+template <class M, int STRAT>
+__global__ void __launch_bounds__(M::NT, min_ctas<M>()) ca_multi_kernel(CaArgs a) {
     __shared__ __align__(16) typename M::Smem sm;
     if (STRAT == TRI_BB) {
         if (blockIdx.x > blockIdx.y + (uint32_t)a.tile_row_begin) return;
@@ -845,36 +936,37 @@ __global__ void __launch_bounds__(Multi<NWV>::NT, NWV == 5 ? 7 : 4) ca_multi_ker
     }
 }
 
-template <int NWV>
-tri_status launch_nw(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
-    constexpr int NT = Multi<NWV>::NT;
+template <class M>
+tri_status launch_geom(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+    constexpr int NT = M::NT;
     if (strategy == TRI_BB) {
         const int64_t tr0 = m.row_begin / m.rho;
         const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;
         if (tr1 <= tr0) return TRI_OK;
         if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
         a.tile_row_begin = tr0;
-        ca_multi_kernel<NWV, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
+        ca_multi_kernel<M, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
     } else if (strategy == TRI_LAMBDA) {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
-        ca_multi_kernel<NWV, TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
+        ca_multi_kernel<M, TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
     } else {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<NWV, TRI_LAMBDA_PERSIST>, NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<M, TRI_LAMBDA_PERSIST>, NT, 0);
         uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
         if (g > nb) g = nb;
-        ca_multi_kernel<NWV, TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
+        ca_multi_kernel<M, TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
     }
     tri::note_launches(1);
     return tri::cuda_status();
 }
 
-
+// rho = 128 (k <= 16) or rho = 224 (k <= 8); the caller has validated (rho, k).
 tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
-    return a.k <= Multi<5>::KMAX ? launch_nw<5>(m, strategy, a, st) : launch_nw<6>(m, strategy, a, st);
+    if (m.rho == G8::RHO) return launch_geom<G8>(m, strategy, a, st);
+    return a.k <= G5::KMAX ? launch_geom<G5>(m, strategy, a, st) : launch_geom<G6>(m, strategy, a, st);
 }
 
 }  // namespace multi
@@ -944,7 +1036,8 @@ tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_
     a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
     a.tile_row_begin = 0;
     switch (m.rho) {
-        case 128: return multi::launch(m, strategy, a, st);        // the k-generation kernel at k = 1
+        case 128:                                                   // the k-generation kernel at k = 1
+        case 224: return multi::launch(m, strategy, a, st);
         case 256: return bits::launch<256>(m, strategy, a, st);
         case 512: return launch_r<512>(m, strategy, a, st);
         default: return TRI_EINVAL;

@@ -107,6 +107,20 @@ def test_map_init_errors(L):
     assert e.value.code == tri.TRI_ERANGE
 
 
+@pytest.mark.parametrize("rho,k,ok", [(128, 16, True), (128, 17, False), (224, 8, True), (224, 9, False),
+                                      (256, 1, False), (224, 0, False)])
+def test_ca_steps_geometry_validation(L, rho, k, ok):
+    """tri_ca_steps accepts (rho = 128, k <= 16) and (rho = 224, k <= 8) only; a bad
+    pair returns EINVAL synchronously, before any launch (fake device pointers)."""
+    import ctypes
+    m = tri.tri_map_init(1000, rho)
+    if ok:
+        return      # a valid pair would launch: covered by the GPU tests
+    rc = L.tri_ca_steps(ctypes.byref(m), 0, k, ctypes.c_void_p(1 << 20), ctypes.c_void_p(2 << 20), None, None,
+                        None, None)
+    assert rc == tri.TRI_EINVAL
+
+
 def test_host_lambda_vs_oracle(L, orc):
     rng = random.Random(5)
     ws = list(range(0, 5000)) + [rng.randrange(0, 2**40) for _ in range(3000)]

@@ -315,7 +315,7 @@ def ca_gpu(n, state, steps, strategy, rho, world=1):
 
 
 @pytest.mark.parametrize("strategy", STRATS)
-@pytest.mark.parametrize("rho", [128, 256, 512])
+@pytest.mark.parametrize("rho", [128, 224, 256, 512])
 @pytest.mark.parametrize("n,seed,steps", [(1, 7, 2), (2, 42, 3), (3, 7, 2), (17, 42, 5), (130, 7, 6),
                                           (1000, 42, 4), (2049, 7, 3)])
 def test_ca_small(orc, strategy, rho, n, seed, steps):
@@ -330,7 +330,7 @@ def test_ca_ranks_with_halos(orc, world):
     assert np.array_equal(ca_gpu(n, st, 5, "lambda", 128, world), orc.ca_run(n, st, 5))
 
 
-@pytest.mark.parametrize("rho", [128, 256, 512])
+@pytest.mark.parametrize("rho", [128, 224, 256, 512])
 @pytest.mark.parametrize("n", [1000, 2049])
 def test_ca_ignores_bytes_past_the_slice(orc, rho, n):
     """State buffers embedded in 0xFF-filled allocations: whatever lies past the
@@ -350,10 +350,10 @@ def test_ca_ignores_bytes_past_the_slice(orc, rho, n):
     assert (bigA[D:] == 255).all() and (bigB[D:] == 255).all()     # nothing written past the slice
 
 
-def ca_steps_gpu(n, state, calls, k, strategy, world=1, fill=None):
+def ca_steps_gpu(n, state, calls, k, strategy, world=1, fill=None, rho=128):
     """`calls` launches of tri_ca_steps(k) per rank, ranks emulated on one GPU with
     deep halos (k packed rows from the owning rank)."""
-    maps = [tri.tri_map_init(n, 128, 1, g, world, 1) for g in range(world)]
+    maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
     full = torch.from_numpy(state).cuda()
 
     def buf(c):
@@ -396,6 +396,29 @@ def test_ca_steps_single(orc, strategy, k, n, seed):
     assert np.array_equal(ca_steps_gpu(n, st, 2, k, strategy), orc.ca_run(n, st, 2 * k))
 
 
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8])
+@pytest.mark.parametrize("n,seed", [(1, 7), (2, 42), (17, 7), (225, 42), (1000, 7), (2049, 42)])
+def test_ca_steps_rho224(orc, strategy, k, n, seed):
+    """The rho = 224 geometry (two words per phase-B thread, 256-column bitmaps)."""
+    st = inputs.ca_state(n, seed)
+    assert np.array_equal(ca_steps_gpu(n, st, 2, k, strategy, rho=224), orc.ca_run(n, st, 2 * k))
+
+
+@pytest.mark.parametrize("world,k,rho", [(2, 4, 224), (3, 8, 224), (4, 3, 224)])
+def test_ca_steps_deep_halo_ranks_rho224(orc, world, k, rho):
+    n = 2000
+    st = inputs.ca_state(n, 42)
+    assert np.array_equal(ca_steps_gpu(n, st, 3, k, "lambda", world, rho=rho), orc.ca_run(n, st, 3 * k))
+
+
+@pytest.mark.parametrize("k", [1, 8])
+def test_ca_steps_ignores_garbage_rho224(orc, k):
+    n = 2049
+    st = inputs.ca_state(n, 7)
+    assert np.array_equal(ca_steps_gpu(n, st, 2, k, "lambda", 1, fill=255, rho=224), orc.ca_run(n, st, 2 * k))
+
+
 @pytest.mark.parametrize("world,k", [(2, 4), (3, 3), (4, 8), (3, 1), (2, 16), (3, 11)])
 def test_ca_steps_deep_halo_ranks(orc, world, k):
     n = 2000
@@ -410,13 +433,13 @@ def test_ca_steps_ignores_garbage(orc, k):
     assert np.array_equal(ca_steps_gpu(n, st, 2, k, "lambda", 1, fill=255), orc.ca_run(n, st, 2 * k))
 
 
-@pytest.mark.parametrize("k", [4, 8, 16])
-def test_ca_steps_full_size_sampled(orc, k):
+@pytest.mark.parametrize("k,rho", [(4, 128), (8, 128), (16, 128), (8, 224)])
+def test_ca_steps_full_size_sampled(orc, k, rho):
     """BASELINE configs[3] (n = 32768) with k-generation launches (the bench's plan uses
     the k it measures fastest), sampled rows."""
     n = 32768
     st = inputs.ca_state(n, 42)
-    m = tri.tri_map_init(n, 128)
+    m = tri.tri_map_init(n, rho)
     a = torch.from_numpy(st).cuda()
     b = torch.empty_like(a)
     tri.tri_ca_steps(m, "lambda", k, a, b)

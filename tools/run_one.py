@@ -48,7 +48,7 @@ def main():
         fn = lambda: tri.tri_ca_step(m, a.strategy, x, y)
     elif w == "ca_steps":
         n = a.n or 32768
-        m = tri.tri_map_init(n, 128)
+        m = tri.tri_map_init(n, a.rho or 128)
         x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
         y = torch.empty_like(x)
         fn = lambda: tri.tri_ca_steps(m, a.strategy, a.k, x, y)
