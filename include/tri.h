@@ -209,6 +209,39 @@ tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const
                         uint8_t *d_out, const uint8_t *d_halo_above, const uint8_t *d_halo_below,
                         void *d_ws, void *stream);
 
+/* tri_ca_steps with the halo exchange fused into the kernel's store phase
+ * (peer-memory halo stores over NVLink instead of a
+ * separate send/recv after the kernel).  Same arguments and result as
+ * tri_ca_steps, plus two destinations the tiles ALSO store to while writing
+ * d_out:
+ *   d_peer_above: the packed rows [row_begin, row_begin + k) of the NEW state,
+ *     at offsets [0, T(row_begin + k) - T(row_begin)) -- i.e. the halo_below
+ *     buffer of the rank owning row row_begin - 1 (ignored when row_begin == 0);
+ *   d_peer_below: a base address such that the packed rows [row_end - k, row_end)
+ *     land at d_peer_below + (T(r) + c - T(row_begin)) -- i.e. the halo_above
+ *     buffer of the rank owning row row_end sits at d_peer_below +
+ *     T(row_end - k) - T(row_begin) (ignored when row_end == n).
+ * Both 16-byte aligned (EINVAL otherwise), device pointers valid in this
+ * context (peer memory opened with tri_ipc_open, or local buffers), or NULL.
+ * A rank owning rows must own >= k of them (EINVAL).  The stores are ordinary
+ * global stores: the caller orders them against the peers' next launch (e.g. a
+ * stream-ordered 4-byte all-reduce per epoch) and double-buffers the halo
+ * buffers by epoch parity so a launch never writes a buffer a peer still reads. */
+tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in,
+                            uint8_t *d_out, const uint8_t *d_halo_above, const uint8_t *d_halo_below,
+                            uint8_t *d_peer_above, uint8_t *d_peer_below, void *d_ws, void *stream);
+
+/* CUDA IPC for the peer buffers of tri_ca_steps_p2p (one process per GPU).
+ * tri_ipc_handle: the TRI_IPC_HANDLE_BYTES-byte handle of the device allocation
+ * holding d_ptr and d_ptr's offset in it (cudaIpcGetMemHandle on the allocation
+ * base).  tri_ipc_open: maps a handle from another process (peer access enabled
+ * lazily); *d_ptr = base + offset, *d_base = the mapping to pass to tri_ipc_close.
+ * ECUDA on any CUDA failure (e.g. a handle opened in the process that made it). */
+#define TRI_IPC_HANDLE_BYTES 64
+tri_status tri_ipc_handle(const void *d_ptr, void *handle, uint64_t *offset);
+tri_status tri_ipc_open(const void *handle, uint64_t offset, void **d_ptr, void **d_base);
+tri_status tri_ipc_close(void *d_base);
+
 /*
  * Tetrahedral map descriptor.  Tiles (i, j, k), j <= i <= k < m,
  * enumerated layer-major (layer k = a triangle of side k+1, Eq. 1 inside).

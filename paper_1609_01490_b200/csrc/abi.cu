@@ -42,6 +42,25 @@ static uint64_t snap_row(uint64_t g, uint64_t world, uint64_t m, uint64_t B) {
     return best > m ? m : best;
 }
 
+// [base, base + size) of the device allocation holding p (cuMemGetAddressRange,
+// resolved through the runtime so the library needs no link-time libcuda).
+static tri_status cuda_driver_range(const void *p, void **base, size_t *size) {
+    typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+    static range_fn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return TRI_ECUDA;
+        fn = (range_fn)f;
+    }
+    unsigned long long b = 0;
+    if (fn(&b, size, (unsigned long long)(uintptr_t)p) != 0) return TRI_ECUDA;
+    *base = (void *)(uintptr_t)b;
+    return TRI_OK;
+}
+
 }  // namespace tri
 
 using namespace tri;
@@ -209,7 +228,55 @@ tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const
     if (k < 1 || !((map->rho == 128 && k <= 16) || (map->rho == 224 && k <= 8))) return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
-    return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);
+    return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, nullptr, nullptr,
+                           (cudaStream_t)stream);
+}
+
+tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in, uint8_t *d_out,
+                            const uint8_t *d_halo_above, const uint8_t *d_halo_below, uint8_t *d_peer_above,
+                            uint8_t *d_peer_below, void *d_ws, void *stream) {
+    g_launches = 0;
+    (void)d_ws;
+    if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
+    if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
+    if (k < 1 || !((map->rho == 128 && k <= 16) || (map->rho == 224 && k <= 8))) return TRI_EINVAL;
+    if ((((uintptr_t)d_in) | ((uintptr_t)d_out) | ((uintptr_t)d_peer_above) | ((uintptr_t)d_peer_below)) & 15u)
+        return TRI_EINVAL;
+    // every peer row this rank sends must be its own: it owns >= k rows (or none)
+    if ((d_peer_above || d_peer_below) && map->row_end > map->row_begin && map->row_end - map->row_begin < k)
+        return TRI_EINVAL;
+    if (map->out_cells == 0) return TRI_OK;
+    return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, d_peer_above, d_peer_below,
+                           (cudaStream_t)stream);
+}
+
+tri_status tri_ipc_handle(const void *d_ptr, void *handle, uint64_t *offset) {
+    if (!d_ptr || !handle || !offset) return TRI_EINVAL;
+    void *base = nullptr;
+    size_t size = 0;
+    if (cuda_driver_range(d_ptr, &base, &size) != TRI_OK) return TRI_ECUDA;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, base) != cudaSuccess) return TRI_ECUDA;
+    static_assert(sizeof(h) == TRI_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (uint64_t)((const char *)d_ptr - (const char *)base);
+    return TRI_OK;
+}
+
+tri_status tri_ipc_open(const void *handle, uint64_t offset, void **d_ptr, void **d_base) {
+    if (!handle || !d_ptr || !d_base) return TRI_EINVAL;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return TRI_ECUDA;
+    *d_base = base;
+    *d_ptr = (char *)base + offset;
+    return TRI_OK;
+}
+
+tri_status tri_ipc_close(void *d_base) {
+    if (!d_base) return TRI_EINVAL;
+    return cudaIpcCloseMemHandle(d_base) == cudaSuccess ? TRI_OK : TRI_ECUDA;
 }
 
 tri_status tet_map_init(tet_map_t *map, int64_t n, int32_t rho, int32_t rank, int32_t world) {

@@ -38,6 +38,10 @@ struct CaArgs {
     uint64_t out_cells;
     uint64_t omega_begin, omega_end;
     int64_t tile_row_begin;
+    // fused halo exchange (tri_ca_steps_p2p; NULL otherwise): rows [R0, R0 + k) are
+    // also stored to peer_above + (slice offset), rows [R1 - k, R1) to peer_below +
+    // (slice offset) -- the neighbours' halo buffers, mapped over NVLink
+    uint8_t *peer_above, *peer_below;
 };
 
 // Row pointer to column 0 of row r, or nullptr for a dead row.
@@ -855,6 +859,7 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
     const int rr_hi = hi64 < 0 ? 0 : (hi64 > RHO ? RHO : (int)hi64);
     const int64_t dr64 = r0 - c0 + 1;                         // seg(rr) = dr + rr cells in the row from c0
     const int dr = dr64 > (1 << 20) ? (1 << 20) : (dr64 < -RHO ? -RHO : (int)dr64);
+    const bool p2p = a.peer_above != nullptr || a.peer_below != nullptr;
     auto chunk = [](uint32_t h) {                             // 16 bits -> 16 bytes {0,1}
         return make_uint4(bits::spread4(h & 15u), bits::spread4((h >> 4) & 15u), bits::spread4((h >> 8) & 15u),
                           bits::spread4((h >> 12) & 15u));
@@ -867,12 +872,30 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
         const uint64_t s = sm.seg[rr];
         const int delta = (int)((0u - (uint32_t)s) & 15u);
         const int y = rr + K;
+        // this row's extra destinations: the neighbours' halo buffers (P2P), when it
+        // is among the first / last k rows of the slice
+        uint8_t *pa = nullptr, *pb = nullptr;
+        if (p2p) {
+            const int64_t r = r0 + rr;
+            pa = r < a.R0 + K ? a.peer_above : nullptr;
+            pb = r >= a.R1 - K ? a.peer_below : nullptr;
+        }
+        auto put16 = [&](uint64_t o, const uint4 v) {
+            st_cs_v4u(a.out + o, v.x, v.y, v.z, v.w);
+            if (pa) st_cs_v4u(pa + o, v.x, v.y, v.z, v.w);
+            if (pb) st_cs_v4u(pb + o, v.x, v.y, v.z, v.w);
+        };
+        auto put1 = [&](uint64_t o, uint8_t v) {
+            a.out[o] = v;
+            if (pa) pa[o] = v;
+            if (pb) pb[o] = v;
+        };
         if (slot == 0 && c0 == 0) {                           // head bytes of the row (c0 = 0 only)
             const int hb = delta < len ? delta : len;
 #pragma unroll 1
             for (int u = 0; u < hb; ++u) {
                 const int x = u + K;
-                a.out[s + u] = (uint8_t)((fin[y][x >> 5] >> (x & 31)) & 1u);
+                put1(s + u, (uint8_t)((fin[y][x >> 5] >> (x & 31)) & 1u));
             }
         }
         const int off = delta + 16 * CPL * slot;              // chunks [off, off + 16) (and [off + 16, off + 32))
@@ -881,25 +904,23 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
         const uint32_t w0 = fin[y][wi];
         const uint32_t w1 = wi + 1 < NW ? fin[y][wi + 1] : 0u;
         const uint32_t b = __funnelshift_r(w0, w1, (uint32_t)(x & 31));   // cells off .. off + 31
-        uint8_t *dst = a.out + s + off;
+        const uint64_t o = s + off;
         const bool second = CPL == 2 && off + 16 < len;       // a second chunk, and it is this tile's
         if (CPL == 2 && second && off + 32 <= seg) {
-            const uint4 v0 = chunk(b), v1 = chunk(b >> 16);
-            st_cs_v4u(dst, v0.x, v0.y, v0.z, v0.w);
-            st_cs_v4u(dst + 16, v1.x, v1.y, v1.z, v1.w);
+            put16(o, chunk(b));
+            put16(o + 16, chunk(b >> 16));
         } else {
             // a chunk crossing the row end: its row-i part only (if the second chunk
             // exists and crosses, the first is full)
             const int end = seg - off < 32 ? seg - off : 32;
             int u = 0;
             if (off + 16 <= seg) {
-                const uint4 v0 = chunk(b);
-                st_cs_v4u(dst, v0.x, v0.y, v0.z, v0.w);
+                put16(o, chunk(b));
                 u = 16;
             }
             if (u == 0 || second) {
 #pragma unroll 1
-                for (; u < end; ++u) dst[u] = (uint8_t)((b >> u) & 1u);
+                for (; u < end; ++u) put1(o + u, (uint8_t)((b >> u) & 1u));
             }
         }
     }
@@ -1031,6 +1052,7 @@ tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_
     a.below = m.row_end < m.n ? below : nullptr;
     a.n = m.n; a.R0 = m.row_begin; a.R1 = m.row_end;
     a.k = 1;
+    a.peer_above = a.peer_below = nullptr;
     a.base = m.out_offset; a.out_cells = m.out_cells;
     a.above_base = m.row_begin > 0 ? T2((uint64_t)m.row_begin - 1) : 0;
     a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
@@ -1045,7 +1067,8 @@ tri_status launch_ca(const tri_map_t &m, int strategy, const uint8_t *in, uint8_
 }
 
 tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,
-                           const uint8_t *above, const uint8_t *below, cudaStream_t st) {
+                           const uint8_t *above, const uint8_t *below, uint8_t *peer_above, uint8_t *peer_below,
+                           cudaStream_t st) {
     if (((uintptr_t)out & 15u) != 0 || ((uintptr_t)in & 15u) != 0) return TRI_EINVAL;
     CaArgs a;
     a.in = in; a.out = out;
@@ -1053,6 +1076,8 @@ tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_
     a.below = m.row_end < m.n ? below : nullptr;
     a.n = m.n; a.R0 = m.row_begin; a.R1 = m.row_end;
     a.k = k;
+    a.peer_above = m.row_begin > 0 ? peer_above : nullptr;
+    a.peer_below = m.row_end < m.n ? peer_below : nullptr;
     a.base = m.out_offset; a.out_cells = m.out_cells;
     const int64_t first_above = m.row_begin - k > 0 ? m.row_begin - k : 0;
     a.above_base = T2((uint64_t)first_above);

@@ -286,7 +286,8 @@ tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream
 tri_status launch_collide1d(const tri_map_t &m, int strategy, const float *iv, unsigned long long *count,
                             cudaStream_t st);
 tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,
-                           const uint8_t *above, const uint8_t *below, cudaStream_t st);
+                           const uint8_t *above, const uint8_t *below, uint8_t *peer_above, uint8_t *peer_below,
+                           cudaStream_t st);
 tri_status launch_edm_rb(const tri_map_t &m, const float *pts, int dim, int64_t ld, float *out, cudaStream_t st);
 tri_status launch_dummy(const tri_map_t &m, int strategy, int mode, void *d_out, cudaStream_t st);
 tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int dim, int64_t ld,

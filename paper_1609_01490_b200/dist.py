@@ -111,3 +111,104 @@ def halo_exchange(state: torch.Tensor, bounds, n: int, rank: int, above: torch.T
     if staged:
         for buf, t in host_recvs:
             t.copy_(buf)
+
+
+# ---------------------------------------------------------------------------
+# Fused halo exchange (tri_ca_steps_p2p): the CA kernel itself stores its first /
+# last k rows into the neighbours' halo buffers over NVLink (CUDA IPC mappings),
+# so an epoch needs no send/recv -- only a stream-ordered 4-byte all-reduce that
+# orders the peer stores before the neighbours' next launch.  Halo buffers are
+# double-buffered by epoch parity: launch e reads its parity-e buffers and writes
+# the neighbours' parity-(e+1) ones, which the neighbours last read in launch e-1
+# (finished, by the all-reduce after it).
+
+def peer_below_shift(bounds, rank: int, k: int) -> int:
+    """T(R1 - k) - T(R0): where the sender's rows [R1 - k, R1) start in its slice."""
+    R0, R1 = bounds[rank]
+    return T(max(R1 - k, R0)) - T(R0)
+
+
+class P2PHalo:
+    """Double-buffered receive buffers of one rank plus the neighbours' buffers it
+    stores into.  ``exchange=True`` swaps CUDA IPC handles over torch.distributed
+    and maps the neighbours' buffers (one process per GPU); ``exchange=False``
+    leaves the peers to ``link`` (ranks emulated in one process, in tests)."""
+
+    def __init__(self, bounds, n: int, rank: int, k: int, device=None, exchange: bool = True):
+        self.bounds, self.n, self.rank, self.k = bounds, n, rank, k
+        R0, R1 = bounds[rank]
+        self.R0, self.R1 = R0, R1
+        self.na, self.nb = halo_bytes(bounds, n, rank, k)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # the above buffer's address must match the sender's store phase mod 16:
+        # the sender writes its slice offset x at (its peer_below) + x, 16-byte aligned
+        g_up = owner(bounds, R0 - 1) if R0 > 0 else None
+        self.phase = (peer_below_shift(bounds, g_up, k) % 16) if g_up is not None else 0
+        self._bufs = [torch.zeros(self.na + 32, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self._belows = [torch.zeros(max(self.nb, 1) + 16, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.above = [b[self.phase:self.phase + max(self.na, 1)] for b in self._bufs]
+        self.below = [b[:max(self.nb, 1)] for b in self._belows]
+        self.peer_above = [None, None]     # addresses in the upper neighbour's below buffers
+        self.peer_below = [None, None]     # base addresses for the lower neighbour's above buffers
+        self._opened = []
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        if exchange:
+            self._exchange()
+
+    def handles(self):
+        from . import tri
+        return {"above": [tri.tri_ipc_handle(t) for t in self.above],
+                "below": [tri.tri_ipc_handle(t) for t in self.below]}
+
+    def link(self, up_below_addrs, down_above_addrs):
+        """Peers given as addresses: the upper neighbour's below buffers and the lower
+        neighbour's above buffers (per parity), or None at the domain edge."""
+        shift = peer_below_shift(self.bounds, self.rank, self.k)
+        for p in range(2):
+            self.peer_above[p] = None if up_below_addrs is None else up_below_addrs[p]
+            self.peer_below[p] = None if down_above_addrs is None else down_above_addrs[p] - shift
+
+    def _exchange(self):
+        from . import tri
+        world = dist.get_world_size()
+        allh = [None] * world
+        dist.all_gather_object(allh, self.handles())
+        up = owner(self.bounds, self.R0 - 1) if self.R0 > 0 and self.R1 > self.R0 else None
+        down = owner(self.bounds, self.R1) if self.R1 < self.n and self.R1 > self.R0 else None
+
+        def open_all(hs):
+            out = []
+            for h, off in hs:
+                ptr, base = tri.tri_ipc_open(h, off)
+                self._opened.append(base)
+                out.append(ptr)
+            return out
+        self.link(open_all(allh[up]["below"]) if up is not None else None,
+                  open_all(allh[down]["above"]) if down is not None else None)
+
+    def close(self):
+        from . import tri
+        for b in self._opened:
+            tri.tri_ipc_close(b)
+        self._opened = []
+
+    def prime(self, state: torch.Tensor):
+        """Parity-0 halos of the initial state (one ordinary exchange)."""
+        halo_exchange(state, self.bounds, self.n, self.rank, self.above[0] if self.R0 > 0 else None,
+                      self.below[0] if self.R1 < self.n else None, self.k)
+
+    def args(self, epoch: int):
+        """(halo_above, halo_below, peer_above, peer_below) for launch ``epoch``."""
+        p, q = epoch % 2, (epoch + 1) % 2
+        return (self.above[p] if self.R0 > 0 else None, self.below[p] if self.R1 < self.n else None,
+                self.peer_above[q], self.peer_below[q])
+
+    def epoch_barrier(self):
+        """Order this launch's peer stores before the neighbours' next launch."""
+        if not (dist.is_initialized() and dist.get_world_size() > 1):
+            return
+        if _gloo():
+            torch.cuda.synchronize()
+            dist.barrier()
+        else:
+            dist.all_reduce(self.flag)          # stream-ordered, 4 bytes

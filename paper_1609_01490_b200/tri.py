@@ -75,6 +75,11 @@ SIGNATURES = {
     "tri_ca_workspace_size": ([ctypes.POINTER(TriMap)], ctypes.c_size_t),
     "tri_ca_step": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_i32),
     "tri_ca_steps": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_i32),
+    "tri_ca_steps_p2p": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+                         c_i32),
+    "tri_ipc_handle": ([c_vp, c_vp, ctypes.POINTER(c_u64)], c_i32),
+    "tri_ipc_open": ([c_vp, c_u64, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)], c_i32),
+    "tri_ipc_close": ([c_vp], c_i32),
     "tet_map_init": ([ctypes.POINTER(TetMap), c_i64, c_i32, c_i32, c_i32], c_i32),
     "tet_lambda": ([c_u64, ctypes.POINTER(c_u32), ctypes.POINTER(c_u32), ctypes.POINTER(c_u32)], c_i32),
     "tet_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
@@ -242,6 +247,45 @@ def tri_ca_steps(m: TriMap, strategy, k, state_in, state_out, halo_above=None, h
     """k generations in one call; halos are the k packed rows on either side."""
     _ok(lib().tri_ca_steps(ctypes.byref(m), _strategy(strategy), int(k), _ptr(state_in), _ptr(state_out),
                            _ptr(halo_above), _ptr(halo_below), _ptr(ws), _stream(stream)), "tri_ca_steps")
+
+
+def _addr(x):
+    """A device address: a tensor's data pointer, a raw int (peer memory from tri_ipc_open), or None."""
+    if x is None or isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def tri_ca_steps_p2p(m: TriMap, strategy, k, state_in, state_out, halo_above=None, halo_below=None,
+                     peer_above=None, peer_below=None, ws=None, stream=None):
+    """tri_ca_steps that also stores its first / last k rows into the neighbours' halo
+    buffers (peer_above / peer_below: addresses as include/tri.h defines them)."""
+    _ok(lib().tri_ca_steps_p2p(ctypes.byref(m), _strategy(strategy), int(k), _ptr(state_in), _ptr(state_out),
+                               _addr(halo_above), _addr(halo_below), _addr(peer_above), _addr(peer_below),
+                               _ptr(ws), _stream(stream)), "tri_ca_steps_p2p")
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def tri_ipc_handle(t) -> tuple[bytes, int]:
+    """(handle bytes, offset of t in its allocation) for another process's tri_ipc_open."""
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    off = c_u64(0)
+    _ok(lib().tri_ipc_handle(ctypes.c_void_p(_addr(t)), h, ctypes.byref(off)), "tri_ipc_handle")
+    return h.raw, int(off.value)
+
+
+def tri_ipc_open(handle: bytes, offset: int) -> tuple[int, int]:
+    """Map another process's allocation: (address of the buffer, mapping base for tri_ipc_close)."""
+    assert len(handle) == IPC_HANDLE_BYTES
+    p, b = c_vp(), c_vp()
+    _ok(lib().tri_ipc_open(handle, c_u64(offset), ctypes.byref(p), ctypes.byref(b)), "tri_ipc_open")
+    return int(p.value), int(b.value)
+
+
+def tri_ipc_close(base: int) -> None:
+    _ok(lib().tri_ipc_close(ctypes.c_void_p(base)), "tri_ipc_close")
 
 
 def tet_triplet(m: TetMap, strategy, pts4, energy, nu=1.0, stream=None):

@@ -121,6 +121,28 @@ def test_ca_steps_geometry_validation(L, rho, k, ok):
     assert rc == tri.TRI_EINVAL
 
 
+def test_ca_steps_p2p_validation(L):
+    """tri_ca_steps_p2p: misaligned peer pointers, a rank owning fewer than k rows and
+    bad (rho, k) pairs are EINVAL before any launch (fake device pointers); the IPC
+    calls reject NULLs."""
+    import ctypes
+    vp = ctypes.c_void_p
+    A, B, P = vp(1 << 20), vp(2 << 20), vp(3 << 20)
+    m = tri.tri_map_init(1000, 128, 1, 1, 2, 1)
+    call = lambda mp, k, pa: L.tri_ca_steps_p2p(ctypes.byref(mp), 0, k, A, B, None, None, pa, None, None, None)
+    assert call(m, 4, vp((3 << 20) + 8)) == tri.TRI_EINVAL          # peer not 16-byte aligned
+    assert call(m, 17, P) == tri.TRI_EINVAL                         # k > 16 at rho = 128
+    small = tri.tri_map_init(230, 224, 1, 1, 2, 1)                  # rank 1 owns rows [224, 230)
+    assert (small.row_begin, small.row_end) == (224, 230)
+    assert call(small, 8, P) == tri.TRI_EINVAL                      # owns 6 < k rows, sends to a peer
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64(0)
+    assert L.tri_ipc_handle(None, h, ctypes.byref(off)) == tri.TRI_EINVAL
+    p, b = vp(), vp()
+    assert L.tri_ipc_open(None, 0, ctypes.byref(p), ctypes.byref(b)) == tri.TRI_EINVAL
+    assert L.tri_ipc_close(None) == tri.TRI_EINVAL
+
+
 def test_host_lambda_vs_oracle(L, orc):
     rng = random.Random(5)
     ws = list(range(0, 5000)) + [rng.randrange(0, 2**40) for _ in range(3000)]

@@ -656,3 +656,113 @@ def test_tet_lut_map_equals_cbrt_map(kmax, shift, w0, count):
     with pytest.raises(tri.TriError) as e:                 # omega + 1 past the table
         tri.tet_map_eval_lut(end - 1, 1, kmax, shift, lut, None, fa)
     assert e.value.code == tri.TRI_ERANGE
+
+
+# --------------------------------------------------------------------------- fused P2P halos
+def _p2p_link(halos, bounds, n):
+    from paper_1609_01490_b200 import dist as tdist
+    for g, h in enumerate(halos):
+        R0, R1 = bounds[g]
+        if R1 <= R0:
+            continue
+        up = tdist.owner(bounds, R0 - 1) if R0 > 0 else None
+        down = tdist.owner(bounds, R1) if R1 < n else None
+        h.link([t.data_ptr() for t in halos[up].below] if up is not None else None,
+               [t.data_ptr() for t in halos[down].above] if down is not None else None)
+
+
+def ca_steps_p2p_gpu(n, state, calls, k, strategy, world, rho):
+    """tri_ca_steps_p2p with ranks emulated on one GPU: every launch stores its first
+    / last k rows straight into the neighbours' (parity-double-buffered) halo
+    buffers; no exchange step between launches."""
+    from paper_1609_01490_b200 import dist as tdist
+    maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+    bounds = [(m.row_begin, m.row_end) for m in maps]
+    halos = [tdist.P2PHalo(bounds, n, g, k, exchange=False) for g in range(world)]
+    _p2p_link(halos, bounds, n)
+    full = torch.from_numpy(state).cuda()
+    cur = [full[m.out_offset:m.out_offset + m.out_cells].clone() if m.out_cells else
+           torch.empty(16, dtype=torch.uint8, device="cuda") for m in maps]
+    nxt = [torch.empty_like(c) for c in cur]
+    for g, (h, m) in enumerate(zip(halos, maps)):           # parity-0 halos = the initial state's rows
+        R0, R1 = bounds[g]
+        if R1 > R0 and R0 > 0:
+            h.above[0][:h.na].copy_(full[T(max(R0 - k, 0)):T(R0)])
+        if R1 > R0 and R1 < n:
+            h.below[0][:h.nb].copy_(full[T(R1):T(min(R1 + k, n))])
+    for e in range(calls):
+        for g, m in enumerate(maps):
+            if m.out_cells:
+                tri.tri_ca_steps_p2p(m, strategy, k, cur[g], nxt[g], *halos[g].args(e))
+        cur, nxt = nxt, cur
+    sync()
+    return np.concatenate([c[:m.out_cells].cpu().numpy() for c, m in zip(cur, maps)])
+
+
+@pytest.mark.parametrize("world,k,rho", [(2, 1, 128), (2, 4, 128), (3, 8, 128), (4, 16, 128), (3, 3, 224),
+                                         (2, 8, 224), (4, 5, 224)])
+def test_ca_steps_p2p_emulated(orc, world, k, rho):
+    n = 2000
+    st = inputs.ca_state(n, 7)
+    assert np.array_equal(ca_steps_p2p_gpu(n, st, 3, k, "lambda", world, rho), orc.ca_run(n, st, 3 * k))
+
+
+def test_ca_steps_p2p_single_rank_is_tri_ca_steps(orc):
+    """world = 1: no peers, the result equals tri_ca_steps."""
+    n = 1000
+    st = inputs.ca_state(n, 42)
+    assert np.array_equal(ca_steps_p2p_gpu(n, st, 2, 8, "lambda", 1, 224), orc.ca_run(n, st, 16))
+
+
+def _p2p_worker(rank, world, port, n, k, rho, calls, q):
+    import os
+    import torch.distributed as dist
+    from paper_1609_01490_b200 import dist as tdist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+        bounds = [(m.row_begin, m.row_end) for m in maps]
+        m = maps[rank]
+        st = inputs.ca_state(n, 7)
+        cur = torch.from_numpy(st[m.out_offset:m.out_offset + m.out_cells].copy()).cuda()
+        nxt = torch.empty_like(cur)
+        h = tdist.P2PHalo(bounds, n, rank, k)          # CUDA IPC: maps the neighbour's buffers
+        h.prime(cur)
+        for e in range(calls):
+            tri.tri_ca_steps_p2p(m, "lambda", k, cur, nxt, *h.args(e))
+            h.epoch_barrier()
+            cur, nxt = nxt, cur
+        torch.cuda.synchronize()
+        q.put((rank, cur.cpu().numpy()))
+        dist.barrier()
+        h.close()
+        dist.destroy_process_group()
+    except Exception as ex:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(ex)))
+
+
+@pytest.mark.parametrize("k,rho", [(4, 128), (8, 224)])
+def test_ca_steps_p2p_two_processes_ipc(orc, k, rho):
+    """Two processes (one GPU here, one per GPU in production) exchange CUDA IPC
+    handles of their halo buffers; the kernels store into each other's memory."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n, world, calls = 1500, 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker, args=(g, world, port, n, k, rho, calls, q)) for g in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for g in range(world):
+        assert not isinstance(got[g], str), got[g]
+    st = inputs.ca_state(n, 7)
+    assert np.array_equal(np.concatenate([got[g] for g in range(world)]), orc.ca_run(n, st, calls * k))
