@@ -4,19 +4,30 @@
 //
 // Tile = rho x rho sphere pairs, coordinate from lambda(omega) or the BB grid.
 // The rho column spheres of the tile are staged in shared memory, each stored
-// twice as (x,x,y,y | z,z,r,r) so two LDS.128 broadcasts yield packed f32x2
-// operands.  Each of the rho/4 threads holds K = 4 row spheres as two f32x2
-// pairs and tests them against every column sphere with the sm_100 packed
-// FADD2 / FMUL2 / FFMA2 instructions (IEEE round-to-nearest per lane, so the
-// result is bit-identical to the scalar sequence the ABI fixes):
+// twice as (-2x,-2x,-2y,-2y | -2z,-2z,-2r,-2r | A',A') so LDS broadcasts yield
+// packed f32x2 operands.  Each of the rho/K threads holds K row spheres (K = 8
+// at rho >= 256, else 4) as K/2 f32x2 pairs and tests them against every column
+// sphere with the sm_100 packed FFMA2 / FADD2 instructions.  The count is the
+// ABI's fixed scalar predicate (reading Q9):
 //   dx = xi - xj, dy, dz;  d2 = fma(dz,dz, fma(dy,dy, dx*dx));  s = ri + rj;  d2 < s*s
-// Counting: hits are rare (~6e-6 of the pairs at the benchmark), so the hot
-// loop keeps only min(d2 - s*s) per 32-column block (fp32 subtraction without
-// FTZ is sign-exact: d2 - s2 < 0 <=> d2 < s2; min ignores NaN), and a block
-// whose minimum is negative is recounted exactly with the scalar predicate.
-// Out-of-range spheres are NaN (every comparison false).  Diagonal tiles use
-// the scalar predicate with the strict filter col < row.  Counts are reduced
-// per warp and CTA; one 64-bit atomic per CTA (skipped if 0).
+// but hits are rare (~6e-6 of the pairs at the benchmark), so the hot loop only
+// FILTERS: per 32-column block each thread keeps a bit per column whose gap
+// (below) is negative for one of its rows, and only flagged columns are
+// recounted with the exact predicate.  The gap is d2 - s^2 expanded around the
+// origin as a 4-D dot product,
+//   d2 - s^2 = A_i + A_j - 2 (x_i x_j + y_i y_j + z_i z_j + r_i r_j),
+//   A = |x|^2 - r^2,
+// evaluated as g = A'_i + fma(x_i, -2x_j, fma(y_i, -2y_j, fma(z_i, -2z_j,
+// fma(r_i, -2r_j, A'_j)))) -- 5 FP32 ops per pair instead of the predicate's 9
+// -- with A' = A - kappa u M, M = |x|^2 + r^2, u = 2^-24, kappa = 64.  The
+// filter's rounding error is <= ~15 u (M_i + M_j) and a pair the fixed-order
+// predicate counts has d2* - s*^2 <= ~10 u (M_i + M_j) in exact arithmetic
+// (first order), so every counted pair has
+// g < (25 - kappa) u (M_i + M_j) < 0: no hit is ever missed, and the count is
+// exactly the predicate's.  The per-sphere A' is computed while staging the
+// tile.  NaN (out-of-range spheres) never flags (min ignores NaN).  Diagonal
+// tiles use the scalar predicate with the strict filter col < row.  Counts are
+// reduced per warp and CTA; one 64-bit atomic per CTA (skipped if 0).
 #include "tri_common.cuh"
 
 namespace {
@@ -70,12 +81,18 @@ __device__ __forceinline__ uint32_t hit(const float4 a, float xj, float yj, floa
     return d2 < __fmul_rn(s, s) ? 1u : 0u;
 }
 
-// d2 - s*s for the two packed row spheres (x, y, z, r) against one column sphere.
-__device__ __forceinline__ f2 gap2(f2 x, f2 y, f2 z, f2 r, f2 cx, f2 cy, f2 cz, f2 cr) {
-    const f2 dx = sub2(x, cx), dy = sub2(y, cy), dz = sub2(z, cz);
-    const f2 d2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
-    const f2 s = add2(r, cr);
-    return sub2(d2, mul2(s, s));
+// A' = |x|^2 - r^2 - kappa u (|x|^2 + r^2): the per-sphere part of the filter gap.
+constexpr float kFilterKappaU = 64.0f / 16777216.0f;     // kappa u = 2^-18
+__device__ __forceinline__ float filter_a(const float4 c) {
+    const float q = fmaf(c.z, c.z, fmaf(c.y, c.y, c.x * c.x));
+    const float w = c.w * c.w;
+    return fmaf(-kFilterKappaU, q + w, q - w);
+}
+
+// filter gap for the two packed row spheres against one column sphere (column
+// values pre-scaled by -2, column A' folded into the start of the chain)
+__device__ __forceinline__ f2 gap2(f2 x, f2 y, f2 z, f2 r, f2 A, f2 cx, f2 cy, f2 cz, f2 cr, f2 cA) {
+    return add2(A, fma2(x, cx, fma2(y, cy, fma2(z, cz, fma2(r, cr, cA)))));
 }
 
 __device__ __forceinline__ float4 load_sphere(const CollideArgs &a, int64_t idx) {
@@ -84,58 +101,84 @@ __device__ __forceinline__ float4 load_sphere(const CollideArgs &a, int64_t idx)
     return make_float4(nan, nan, nan, nan);
 }
 
-constexpr int K = 4;          // row spheres per thread
+// row spheres per thread: 8 (one column load serves 8 rows) where that still leaves a
+// full warp per CTA (rho >= 256), else 4
+template <int RHO> constexpr int rows_per_thread() { return RHO >= 256 ? 8 : 4; }
 constexpr int BLK = 32;       // columns per min-block
 
+struct ColSmem {
+    float4 c[2];          // (-2x, -2x, -2y, -2y), (-2z, -2z, -2r, -2r)
+    float2 a;             // (A', A')
+};
+
 template <int RHO>
-__device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t bi, uint32_t bj,
-                                                 float4 (*smem)[2]) {
+__device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t bi, uint32_t bj, ColSmem *smem) {
+    constexpr int K = rows_per_thread<RHO>();
     constexpr int NT = RHO / K;
     const int t = threadIdx.x;
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
 #pragma unroll
     for (int q = 0; q < K; ++q) {
         const float4 c = load_sphere(a, c0 + t + q * NT);
-        smem[t + q * NT][0] = make_float4(c.x, c.x, c.y, c.y);
-        smem[t + q * NT][1] = make_float4(c.z, c.z, c.w, c.w);
+        const float A = filter_a(c);
+        smem[t + q * NT].c[0] = make_float4(-2.f * c.x, -2.f * c.x, -2.f * c.y, -2.f * c.y);
+        smem[t + q * NT].c[1] = make_float4(-2.f * c.z, -2.f * c.z, -2.f * c.w, -2.f * c.w);
+        smem[t + q * NT].a = make_float2(A, A);
     }
     float4 R[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) R[q] = load_sphere(a, r0 + t + q * NT);
     __syncthreads();
     uint32_t cnt = 0;
+    // the exact predicate against column c (its coordinates recovered exactly: -2x * -0.5)
+    auto recount = [&](int c, uint32_t strict_row_base) {
+        const float4 u = smem[c].c[0], v = smem[c].c[1];
+        const float xj = -0.5f * u.x, yj = -0.5f * u.z, zj = -0.5f * v.x, rj = -0.5f * v.z;
+        uint32_t h = 0;
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            h += ((uint32_t)c < strict_row_base + (uint32_t)(q * NT)) ? hit(R[q], xj, yj, zj, rj) : 0u;
+        return h;
+    };
     if (bi != bj) {
-        const f2 xa = pk(R[0].x, R[1].x), ya = pk(R[0].y, R[1].y), za = pk(R[0].z, R[1].z), ra = pk(R[0].w, R[1].w);
-        const f2 xb = pk(R[2].x, R[3].x), yb = pk(R[2].y, R[3].y), zb = pk(R[2].z, R[3].z), rb = pk(R[2].w, R[3].w);
+        constexpr int G = K / 2;                          // packed row-sphere pairs per thread
+        f2 X[G], Y[G], Z[G], Q[G], A[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float4 p0 = R[2 * g], p1 = R[2 * g + 1];
+            X[g] = pk(p0.x, p1.x); Y[g] = pk(p0.y, p1.y); Z[g] = pk(p0.z, p1.z); Q[g] = pk(p0.w, p1.w);
+            A[g] = pk(filter_a(p0), filter_a(p1));
+        }
 #pragma unroll 1
         for (int cb = 0; cb < RHO; cb += BLK) {
-            float m = __int_as_float(0x7f800000);   // +inf
-#pragma unroll 8
-            for (int c = cb; c < cb + BLK; ++c) {
-                const float4 u = smem[c][0], v = smem[c][1];
-                const f2 cx = pk(u.x, u.y), cy = pk(u.z, u.w), cz = pk(v.x, v.y), cr = pk(v.z, v.w);
-                float g0, g1, g2, g3;
-                upk(gap2(xa, ya, za, ra, cx, cy, cz, cr), g0, g1);
-                upk(gap2(xb, yb, zb, rb, cx, cy, cz, cr), g2, g3);
-                m = fminf(m, fminf(fminf(g0, g1), fminf(g2, g3)));
-            }
-            if (__any_sync(0xffffffffu, m < 0.f)) {
-                if (m < 0.f) {                        // rare: exact recount of this block
-                    for (int c = cb; c < cb + BLK; ++c) {
-                        const float4 u = smem[c][0], v = smem[c][1];
+            uint32_t flags = 0;                           // bit c: some row of this thread flags column cb + c
 #pragma unroll
-                        for (int q = 0; q < K; ++q) cnt += hit(R[q], u.x, u.z, v.x, v.z);
-                    }
+            for (int c = 0; c < BLK; ++c) {
+                const float4 u = smem[cb + c].c[0], v = smem[cb + c].c[1];
+                const float2 w = smem[cb + c].a;
+                const f2 cx = pk(u.x, u.y), cy = pk(u.z, u.w), cz = pk(v.x, v.y), cr = pk(v.z, v.w), cA = pk(w.x, w.y);
+                float mc = __int_as_float(0x7f800000);    // +inf
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float g0, g1;
+                    upk(gap2(X[g], Y[g], Z[g], Q[g], A[g], cx, cy, cz, cr, cA), g0, g1);
+                    mc = fminf(mc, fminf(g0, g1));
+                }
+                flags |= mc < 0.f ? (1u << c) : 0u;
+            }
+            if (__any_sync(0xffffffffu, flags != 0)) {
+                // rare: the exact predicate on the flagged columns only
+#pragma unroll 1
+                while (flags) {
+                    const int c = __ffs(flags) - 1;
+                    flags &= flags - 1;
+                    cnt += recount(cb + c, 0xffffffffu - (uint32_t)(K * NT));
                 }
             }
         }
     } else {  // diagonal tile: strict lower triangle, col < row (scalar, exact)
 #pragma unroll 4
-        for (int c = 0; c < RHO; ++c) {
-            const float4 u = smem[c][0], v = smem[c][1];
-#pragma unroll
-            for (int q = 0; q < K; ++q) cnt += (c < t + q * NT) ? hit(R[q], u.x, u.z, v.x, v.z) : 0u;
-        }
+        for (int c = 0; c < RHO; ++c) cnt += recount(c, (uint32_t)t);
     }
     __syncthreads();  // smem reused by the next tile (persistent form)
     return cnt;
@@ -156,8 +199,8 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, unsigned long long *ds
 }
 
 template <int RHO, int STRAT>
-__global__ void __launch_bounds__(RHO / K) collide_kernel(CollideArgs a) {
-    __shared__ __align__(16) float4 smem[RHO][2];
+__global__ void __launch_bounds__(RHO / rows_per_thread<RHO>()) collide_kernel(CollideArgs a) {
+    __shared__ __align__(16) ColSmem smem[RHO];
     uint32_t cnt = 0;
     if (STRAT == TRI_BB) {
         const uint32_t bj = blockIdx.x;
@@ -175,12 +218,12 @@ __global__ void __launch_bounds__(RHO / K) collide_kernel(CollideArgs a) {
         for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next())
             cnt += collide_tile<RHO>(a, t.bi, t.bj, smem);
     }
-    flush_count<RHO / K>(cnt, a.count);
+    flush_count<RHO / rows_per_thread<RHO>()>(cnt, a.count);
 }
 
 template <int RHO>
 tri_status launch_r(const tri_map_t &m, int strategy, CollideArgs a, cudaStream_t st) {
-    constexpr int NT = RHO / K;
+    constexpr int NT = RHO / rows_per_thread<RHO>();
     if (strategy == TRI_BB) {
         const int64_t tr0 = m.row_begin / m.rho;
         const int64_t tr1 = (m.row_end + m.rho - 1) / m.rho;

@@ -277,6 +277,43 @@ def test_collide_quantized_and_ranks(orc):
     assert tot == ref
 
 
+def _near_touching(n, seed, offset, scale):
+    """n/2 random spheres and, n/2 indices later, a partner at distance (r_i + r_j)(1 + delta),
+    delta within a few fp32 ulps of 0 (both signs): pairs on the predicate's knife edge, in
+    off-diagonal tiles, around an offset origin (large |x| stresses the filter's margin)."""
+    rng = np.random.default_rng(seed)
+    h = n // 2
+    c = rng.random((h, 3)) * scale + offset
+    r = rng.random(h) * 0.01 * scale
+    rp = rng.random(h) * 0.01 * scale
+    d = rng.normal(size=(h, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    delta = rng.integers(-8, 9, size=h) * 2.0 ** -24
+    p = c + d * ((r + rp) * (1 + delta))[:, None]
+    s = np.zeros((2 * h, 4), np.float32)
+    s[:h, :3], s[:h, 3] = c, r
+    s[h:, :3], s[h:, 3] = p, rp
+    return s
+
+
+@pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (0.5, 1.0), (100.0, 1.0), (-1000.0, 10.0), (0.0, 1e-3)])
+def test_collide_knife_edge_pairs(orc, offset, scale):
+    """The hot loop only filters (a 4-D dot-product gap with a rounding margin) and
+    recounts flagged blocks with the fixed-order predicate: pairs within a few ulps of
+    touching, at any coordinate magnitude, must be counted exactly as the oracle does."""
+    s = _near_touching(8192, 11, offset, scale)
+    ref = orc.collide(s)
+    assert ref > 100            # the construction really puts pairs on both sides of the edge
+    d = torch.from_numpy(s).cuda()
+    for rho in (128, 256, 512):
+        for strategy in STRATS:
+            m = tri.tri_map_init(len(s), rho)
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            tri.tri_collide(m, strategy, d, cnt)
+            sync()
+            assert cnt.item() == ref, (rho, strategy)
+
+
 def test_collide_full_size_rank_slice(orc):
     """BASELINE configs[2] (n = 200000): one 64-way snapped rank slice vs the oracle rows."""
     n = 200000
