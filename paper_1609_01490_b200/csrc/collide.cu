@@ -3,11 +3,12 @@
 // radius inside a unit box ... using a shared memory approach").
 //
 // Tile = rho x rho sphere pairs, coordinate from lambda(omega) or the BB grid.
-// The rho column spheres of the tile are staged in shared memory, each stored
-// twice as (-2x,-2x,-2y,-2y | -2z,-2z,-2r,-2r | A',A') so LDS broadcasts yield
-// packed f32x2 operands.  Each of the rho/K threads holds K row spheres (K = 8
-// at rho >= 256, else 4) as K/2 f32x2 pairs and tests them against every column
-// sphere with the sm_100 packed FFMA2 / FADD2 instructions.  The count is the
+// The rho column spheres of the tile are staged in shared memory as five
+// arrays (-2x, -2y, -2z, -2r, A'): an aligned LDS.128 of one array is two packed
+// f32x2 operands (columns c, c+1 and c+2, c+3), 20 B per sphere.  Each of the
+// rho/K threads holds K row spheres (K = 8 at rho >= 256, else 4), each
+// duplicated into both halves of an f32x2, and tests them against every column
+// pair with the sm_100 packed FFMA2 / FADD2 instructions.  The count is the
 // ABI's fixed scalar predicate (reading Q9):
 //   dx = xi - xj, dy, dz;  d2 = fma(dz,dz, fma(dy,dy, dx*dx));  s = ri + rj;  d2 < s*s
 // but hits are rare (~6e-6 of the pairs at the benchmark), so the hot loop only
@@ -101,18 +102,16 @@ __device__ __forceinline__ float4 load_sphere(const CollideArgs &a, int64_t idx)
     return make_float4(nan, nan, nan, nan);
 }
 
-// row spheres per thread: 8 (one column load serves 8 rows) where that still leaves a
-// full warp per CTA (rho >= 256), else 4
+// row spheres per thread
 template <int RHO> constexpr int rows_per_thread() { return RHO >= 256 ? 8 : 4; }
-constexpr int BLK = 32;       // columns per min-block
+constexpr int BLK = 32;       // columns per flag block
 
-struct ColSmem {
-    float4 c[2];          // (-2x, -2x, -2y, -2y), (-2z, -2z, -2r, -2r)
-    float2 a;             // (A', A')
-};
+// column spheres, structure of arrays: -2x, -2y, -2z, -2r and A' (20 B per sphere);
+// an aligned float4 of one array is two packed f32x2 operands (columns c, c+1 | c+2, c+3)
+template <int RHO> struct ColSmemT { float v[5][RHO]; };
 
 template <int RHO>
-__device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t bi, uint32_t bj, ColSmem *smem) {
+__device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t bi, uint32_t bj, ColSmemT<RHO> &sm) {
     constexpr int K = rows_per_thread<RHO>();
     constexpr int NT = RHO / K;
     const int t = threadIdx.x;
@@ -120,20 +119,17 @@ __device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t 
 #pragma unroll
     for (int q = 0; q < K; ++q) {
         const float4 c = load_sphere(a, c0 + t + q * NT);
-        const float A = filter_a(c);
-        smem[t + q * NT].c[0] = make_float4(-2.f * c.x, -2.f * c.x, -2.f * c.y, -2.f * c.y);
-        smem[t + q * NT].c[1] = make_float4(-2.f * c.z, -2.f * c.z, -2.f * c.w, -2.f * c.w);
-        smem[t + q * NT].a = make_float2(A, A);
+        const int j = t + q * NT;
+        sm.v[0][j] = -2.f * c.x; sm.v[1][j] = -2.f * c.y; sm.v[2][j] = -2.f * c.z; sm.v[3][j] = -2.f * c.w;
+        sm.v[4][j] = filter_a(c);
     }
     float4 R[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) R[q] = load_sphere(a, r0 + t + q * NT);
     __syncthreads();
     uint32_t cnt = 0;
-    // the exact predicate against column c (its coordinates recovered exactly: -2x * -0.5)
     auto recount = [&](int c, uint32_t strict_row_base) {
-        const float4 u = smem[c].c[0], v = smem[c].c[1];
-        const float xj = -0.5f * u.x, yj = -0.5f * u.z, zj = -0.5f * v.x, rj = -0.5f * v.z;
+        const float xj = -0.5f * sm.v[0][c], yj = -0.5f * sm.v[1][c], zj = -0.5f * sm.v[2][c], rj = -0.5f * sm.v[3][c];
         uint32_t h = 0;
 #pragma unroll
         for (int q = 0; q < K; ++q)
@@ -141,33 +137,41 @@ __device__ __forceinline__ uint32_t collide_tile(const CollideArgs &a, uint32_t 
         return h;
     };
     if (bi != bj) {
-        constexpr int G = K / 2;                          // packed row-sphere pairs per thread
-        f2 X[G], Y[G], Z[G], Q[G], A[G];
+        f2 X[K], Y[K], Z[K], Q[K], A[K];                  // each row duplicated in both halves
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float4 p0 = R[2 * g], p1 = R[2 * g + 1];
-            X[g] = pk(p0.x, p1.x); Y[g] = pk(p0.y, p1.y); Z[g] = pk(p0.z, p1.z); Q[g] = pk(p0.w, p1.w);
-            A[g] = pk(filter_a(p0), filter_a(p1));
+        for (int k = 0; k < K; ++k) {
+            X[k] = pk(R[k].x, R[k].x); Y[k] = pk(R[k].y, R[k].y); Z[k] = pk(R[k].z, R[k].z);
+            Q[k] = pk(R[k].w, R[k].w);
+            const float Ak = filter_a(R[k]);
+            A[k] = pk(Ak, Ak);
         }
 #pragma unroll 1
         for (int cb = 0; cb < RHO; cb += BLK) {
-            uint32_t flags = 0;                           // bit c: some row of this thread flags column cb + c
+            uint32_t flags = 0;
 #pragma unroll
-            for (int c = 0; c < BLK; ++c) {
-                const float4 u = smem[cb + c].c[0], v = smem[cb + c].c[1];
-                const float2 w = smem[cb + c].a;
-                const f2 cx = pk(u.x, u.y), cy = pk(u.z, u.w), cz = pk(v.x, v.y), cr = pk(v.z, v.w), cA = pk(w.x, w.y);
-                float mc = __int_as_float(0x7f800000);    // +inf
+            for (int c = 0; c < BLK; c += 4) {
+                const float4 vx = *reinterpret_cast<const float4 *>(&sm.v[0][cb + c]);
+                const float4 vy = *reinterpret_cast<const float4 *>(&sm.v[1][cb + c]);
+                const float4 vz = *reinterpret_cast<const float4 *>(&sm.v[2][cb + c]);
+                const float4 vr = *reinterpret_cast<const float4 *>(&sm.v[3][cb + c]);
+                const float4 va = *reinterpret_cast<const float4 *>(&sm.v[4][cb + c]);
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    float g0, g1;
-                    upk(gap2(X[g], Y[g], Z[g], Q[g], A[g], cx, cy, cz, cr, cA), g0, g1);
-                    mc = fminf(mc, fminf(g0, g1));
+                for (int h = 0; h < 2; ++h) {
+                    const f2 cx = h ? pk(vx.z, vx.w) : pk(vx.x, vx.y), cy = h ? pk(vy.z, vy.w) : pk(vy.x, vy.y);
+                    const f2 cz = h ? pk(vz.z, vz.w) : pk(vz.x, vz.y), cr = h ? pk(vr.z, vr.w) : pk(vr.x, vr.y);
+                    const f2 cA = h ? pk(va.z, va.w) : pk(va.x, va.y);
+                    float mlo = __int_as_float(0x7f800000), mhi = mlo;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        float glo, ghi;
+                        upk(gap2(X[k], Y[k], Z[k], Q[k], A[k], cx, cy, cz, cr, cA), glo, ghi);
+                        mlo = fminf(mlo, glo);
+                        mhi = fminf(mhi, ghi);
+                    }
+                    flags |= (mlo < 0.f ? (1u << (c + 2 * h)) : 0u) | (mhi < 0.f ? (2u << (c + 2 * h)) : 0u);
                 }
-                flags |= mc < 0.f ? (1u << c) : 0u;
             }
             if (__any_sync(0xffffffffu, flags != 0)) {
-                // rare: the exact predicate on the flagged columns only
 #pragma unroll 1
                 while (flags) {
                     const int c = __ffs(flags) - 1;
@@ -200,7 +204,7 @@ __device__ __forceinline__ void flush_count(uint32_t cnt, unsigned long long *ds
 
 template <int RHO, int STRAT>
 __global__ void __launch_bounds__(RHO / rows_per_thread<RHO>()) collide_kernel(CollideArgs a) {
-    __shared__ __align__(16) ColSmem smem[RHO];
+    __shared__ __align__(16) ColSmemT<RHO> smem;
     uint32_t cnt = 0;
     if (STRAT == TRI_BB) {
         const uint32_t bj = blockIdx.x;
