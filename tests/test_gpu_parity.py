@@ -651,6 +651,31 @@ def test_collide1d_ranks_and_quantized(orc):
         assert tot == orc.collide1d(iv)
 
 
+@pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (100.0, 1.0), (-3000.0, 10.0), (0.0, 1e-4)])
+def test_collide1d_knife_edge_pairs(orc, offset, scale):
+    """The 1-D hot loop only filters on widened end points; partners placed at
+    |ci - cj| = (ri + rj)(1 + delta), delta within a few ulps, must be counted exactly."""
+    rng = np.random.default_rng(3)
+    h = 4096
+    c = rng.random(h) * scale + offset
+    r = rng.random(h) * 1e-3 * scale
+    rp = rng.random(h) * 1e-3 * scale
+    sign = np.where(rng.random(h) < 0.5, -1.0, 1.0)
+    delta = rng.integers(-8, 9, size=h) * 2.0 ** -24
+    iv = np.zeros((2 * h, 2), np.float32)
+    iv[:h, 0], iv[:h, 1] = c, r
+    iv[h:, 0], iv[h:, 1] = c + sign * (r + rp) * (1 + delta), rp
+    ref = orc.collide1d(iv)
+    assert ref > 100
+    d = torch.from_numpy(iv).cuda()
+    for strategy in ("lambda", "bb"):
+        m = tri.tri_map_init(len(iv), 256)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tri.tri_collide1d(m, strategy, d, cnt)
+        sync()
+        assert cnt.item() == ref, strategy
+
+
 # ============================================================== succinct LUT tetrahedral map (P:705-709)
 @pytest.mark.parametrize("shift", [0, 4, 9, 40])
 def test_tet_lut_map_matches_enumeration(orc, shift):

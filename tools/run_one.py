@@ -1,6 +1,6 @@
 """Run one hot-path kernel a few times (for ncu captures and quick sweeps).
 
-python tools/run_one.py edm|dummy|collide|ca|ca_steps|triplet [--rho R] [--strategy S] [--reps K] [--n N]
+python tools/run_one.py edm|dummy|collide|collide1d|ca|ca_steps|triplet [--rho R] [--strategy S] [--reps K] [--n N]
 Prints per-launch CUDA-event times (ms).  Product path only (no oracle)."""
 import argparse
 import os
@@ -52,6 +52,12 @@ def main():
         x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
         y = torch.empty_like(x)
         fn = lambda: tri.tri_ca_steps(m, a.strategy, a.k, x, y)
+    elif w == "collide1d":
+        n = a.n or 200000
+        m = tri.tri_map_init(n, 256)
+        x = torch.from_numpy(inputs.intervals(n, 42, 1e-5)).cuda()
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        fn = lambda: tri.tri_collide1d(m, a.strategy, x, cnt)
     elif w == "triplet":
         n = a.n or 4096
         m = tri.tet_map_init(n, a.rho or 16)
