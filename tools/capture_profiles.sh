@@ -10,9 +10,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 cap() { name=$1; shift; ncu --set full --clock-control none --import-source on -s 1 -c 1 -o gpurun_out/$name -f \
         python tools/run_one.py "$@" --reps 1 > gpurun_out/$name.log 2>&1; }
 cap edm edm --rho 128 --strategy lambda
-cap collide collide --rho 128 --strategy lambda
+cap collide collide --rho 256 --strategy lambda
+cap collide1d collide1d --strategy lambda
 cap ca ca --rho 128 --strategy lambda
-cap ca_multi ca_steps --k 8 --strategy lambda
+cap ca_multi ca_steps --rho 224 --k 8 --strategy lambda
 cap triplet triplet --rho 32 --strategy lambda
 cap dummy dummy --rho 16 --strategy lambda
 ls -la gpurun_out
