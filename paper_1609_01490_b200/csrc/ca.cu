@@ -934,7 +934,9 @@ using G8 = Multi<224, 8, 2, 8>;     // rho = 224, k <= 8
 
 // G5: 7 CTAs per SM (40 registers, a few spills) hide more of phase A's load
 // latency than 5 CTAs without spills: 0.270 -> 0.250 ms at K = 1, n = 32768.
-template <class M> constexpr int min_ctas() { return M::NW == 5 ? 7 : (M::NW == 6 ? 4 : 4); }
+// G8: likewise 5 CTAs (48 registers) over 4 (64) and 3 (80): 0.400 -> 0.376 -> 0.356 ms
+// per 8 generations (the first two steps measured before the store-phase rework).
+template <class M> constexpr int min_ctas() { return M::NW == 5 ? 7 : (M::NW == 6 ? 4 : 5); }
 
 template <class M, int STRAT>
 __global__ void __launch_bounds__(M::NT, min_ctas<M>()) ca_multi_kernel(CaArgs a) {

@@ -169,10 +169,21 @@ class P2PHalo:
             self.peer_below[p] = None if down_above_addrs is None else down_above_addrs[p] - shift
 
     def _exchange(self):
+        """Collective and failure-safe: every rank takes part in both gathers and, if
+        any rank failed to export or map a handle, every rank raises (none is left
+        waiting in a collective)."""
         from . import tri
         world = dist.get_world_size()
+        try:
+            mine, err = self.handles(), None
+        except Exception as ex:  # noqa: BLE001 -- reported to every rank below
+            mine, err = None, repr(ex)
         allh = [None] * world
-        dist.all_gather_object(allh, self.handles())
+        dist.all_gather_object(allh, (mine, err))
+        bad = [e for _, e in allh if e]
+        if bad:
+            raise RuntimeError(f"CUDA IPC handle export failed: {bad[0]}")
+        allh = [h for h, _ in allh]
         up = owner(self.bounds, self.R0 - 1) if self.R0 > 0 and self.R1 > self.R0 else None
         down = owner(self.bounds, self.R1) if self.R1 < self.n and self.R1 > self.R0 else None
 
@@ -183,8 +194,18 @@ class P2PHalo:
                 self._opened.append(base)
                 out.append(ptr)
             return out
-        self.link(open_all(allh[up]["below"]) if up is not None else None,
-                  open_all(allh[down]["above"]) if down is not None else None)
+        try:
+            self.link(open_all(allh[up]["below"]) if up is not None else None,
+                      open_all(allh[down]["above"]) if down is not None else None)
+            err = None
+        except Exception as ex:  # noqa: BLE001
+            err = repr(ex)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        bad = [e for e in errs if e]
+        if bad:
+            self.close()
+            raise RuntimeError(f"CUDA IPC mapping failed: {bad[0]}")
 
     def close(self):
         from . import tri
