@@ -44,18 +44,6 @@ constexpr int kWarps = kEdmThreads / 32;
 // ownership is consistent across tiles.
 template <int RHO> struct ChunkW { static constexpr int CW = RHO == 256 ? 8 : 4; };
 
-template <int DIM, int WN>
-__device__ __forceinline__ float dist_w(const float (&p)[DIM], const float (&w)[DIM][WN], int t) {
-    const float dx = p[0] - w[0][t];
-    float d2 = dx * dx;
-#pragma unroll
-    for (int d = 1; d < DIM; ++d) {
-        const float dd = p[d] - w[d][t];
-        d2 = fmaf(dd, dd, d2);
-    }
-    return sqrt_approx(d2);
-}
-
 template <int DIM>
 __device__ __forceinline__ float dist_gmem(const EdmArgs &a, int64_t i, int64_t j) {
     float d2 = 0.f;
@@ -79,70 +67,11 @@ __device__ __forceinline__ void store_chunk(float *dst, const float (&v)[CW]) {
     else st_cs_v4(dst, v[0], v[1], v[2], v[3]);
 }
 
-// one lane's chunk at window offset D (the row's phase delta)
-template <int DIM, int CW, int D>
-__device__ __forceinline__ void chunk_at(const float (&p)[DIM], const float (&w)[DIM][2 * CW - 1], float *dst) {
-    float v[CW];
-#pragma unroll
-    for (int e = 0; e < CW; ++e) v[e] = dist_w<DIM, 2 * CW - 1>(p, w, D + e);
-    store_chunk<CW>(dst, v);
-}
-
-// warp-uniform dispatch on delta in [0, CW)
-template <int DIM, int CW, int D = 0>
-__device__ __forceinline__ void chunk_phase(int delta, const float (&p)[DIM], const float (&w)[DIM][2 * CW - 1],
-                                            float *dst) {
-    if (delta == D) {
-        chunk_at<DIM, CW, D>(p, w, dst);
-    } else if constexpr (D + 1 < CW) {
-        chunk_phase<DIM, CW, D + 1>(delta, p, w, dst);
-    }
-}
-
-// Interior tile: rows [r0, r0+RHO) x cols [c0, c0+RHO), c0 + RHO < r0.
-// One warp per row segment: lane k owns chunk k (RHO = 32 CW).
-template <int RHO, int DIM>
-__device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, int64_t c0) {
-    constexpr int CW = ChunkW<RHO>::CW, WN = 2 * CW - 1;
-    static_assert(RHO == 32 * CW, "one chunk per lane per row");
-    constexpr int ROWS = RHO / kWarps;            // rows per warp (<= 32)
-    static_assert(ROWS <= 32, "row points are broadcast from one lane each");
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t rbase = r0 + (int64_t)warp * ROWS;
-    if (rbase >= a.n) return;
-    float w[DIM][WN];
-#pragma unroll
-    for (int t = 0; t < WN; ++t) {
-        const int64_t col = c0 + CW * lane + t;               // < r0: always a valid point
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) w[d][t] = __ldg(a.pts + col * a.ld + d);
-    }
-    float pr[DIM];
-    {
-        const int64_t rr = rbase + (lane < ROWS ? lane : 0);
-        const bool in = rr < a.n;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) pr[d] = in ? __ldg(a.pts + rr * a.ld + d) : 0.f;
-    }
-    const int nrows = (int)((a.n - rbase) < ROWS ? (a.n - rbase) : ROWS);
-    uint64_t s = tri::T2((uint64_t)rbase) + (uint64_t)c0 - a.out_offset;   // local start of row rbase
-    float *base = a.out + CW * lane;
-#pragma unroll 1
-    for (int rr = 0; rr < nrows; ++rr) {
-        float p[DIM];
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) p[d] = __shfl_sync(0xffffffffu, pr[d], rr);
-        const int delta = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1));
-        chunk_phase<DIM, CW>(delta, p, w, base + (s + (uint64_t)delta));
-        s += (uint64_t)(rbase + rr + 1);               // T(i+1) = T(i) + i + 1
-    }
-}
-
-// Interior tile at rho = 128 (CW = 4) with the sm_100 packed f32x2 ops: the lane's
-// window is kept as the six overlapping column pairs (w_k, w_k+1), so for every row
-// phase delta the chunk's four cells are two aligned pairs; per chunk 3 FADD2 + 1
-// FMUL2 + 2 FFMA2 per pair instead of 12 + 4 + 8 scalar ops.  Same operation order
-// per lane as dist_w (IEEE per lane): bit-identical results.
+// Interior tile with the sm_100 packed f32x2 ops: two cells per FADD2 / FMUL2 /
+// FFMA2 (the row coordinate a broadcast operand, the window columns paired by
+// the compiler), per 3-D cell pair 3 + 1 + 2 instructions instead of 12 scalar
+// ones.  Same operation order per lane as dist_gmem (dx*dx, then fma per further
+// coordinate; IEEE per lane): bit-identical to the checked path.
 typedef unsigned long long f2;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {
     f2 r;
@@ -168,41 +97,70 @@ __device__ __forceinline__ f2 fma_x2(f2 a, f2 b, f2 c) {
     return r;
 }
 
-template <int DIM, int D>
-__device__ __forceinline__ void chunk_x2(const f2 (&P)[DIM], const f2 (&W)[DIM][6], float *dst) {
-    float v[4];
+// Column pairs (w_k, w_k+1) of the lane's window for the chunk at phase D: from the
+// NP pairs precomputed per tile (CW = 4: all six fit in registers; without them
+// ptxas rebuilds the odd-phase pairs with moves every row, 1.296 -> 1.382 ms), or
+// built in place (CW = 8: fourteen pairs per coordinate would not fit).
+template <int DIM, int CW, int NP>
+struct Window {
+    float w[DIM][2 * CW - 1];
+    f2 W[DIM][NP > 0 ? NP : 1];
+    __device__ __forceinline__ f2 pair(int d, int k) const {
+        if constexpr (NP > 0) return W[d][k];
+        else return pk2(w[d][k], w[d][k + 1]);
+    }
+};
+
+template <int DIM, int CW, int NP, int D>
+__device__ __forceinline__ void chunk_x2(const f2 (&P)[DIM], const Window<DIM, CW, NP> &win, float *dst) {
+    float v[CW];
 #pragma unroll
-    for (int e = 0; e < 4; e += 2) {
+    for (int e = 0; e < CW; e += 2) {
         f2 d2 = 0ull;
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
-            const f2 dd = sub_x2(P[d], W[d][D + e]);
+            const f2 dd = sub_x2(P[d], win.pair(d, D + e));
             d2 = d == 0 ? mul_x2(dd, dd) : fma_x2(dd, dd, d2);
         }
         upk2(d2, v[e], v[e + 1]);
     }
-    st_cs_v4(dst, sqrt_approx(v[0]), sqrt_approx(v[1]), sqrt_approx(v[2]), sqrt_approx(v[3]));
+#pragma unroll
+    for (int e = 0; e < CW; ++e) v[e] = sqrt_approx(v[e]);
+    store_chunk<CW>(dst, v);
 }
 
-template <int DIM>
+template <int DIM, int CW, int NP, int D = 0>
+__device__ __forceinline__ void chunk_phase_x2(int delta, const f2 (&P)[DIM], const Window<DIM, CW, NP> &win,
+                                               float *dst) {
+    if (delta == D) {
+        chunk_x2<DIM, CW, NP, D>(P, win, dst);
+    } else if constexpr (D + 1 < CW) {
+        chunk_phase_x2<DIM, CW, NP, D + 1>(delta, P, win, dst);
+    }
+}
+
+template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile_interior_x2(const EdmArgs &a, int64_t r0, int64_t c0) {
-    constexpr int RHO = 128, CW = 4, WN = 7;
+    constexpr int CW = ChunkW<RHO>::CW, WN = 2 * CW - 1;
+    static_assert(RHO == 32 * CW, "one chunk per lane per row");
     constexpr int ROWS = RHO / kWarps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t rbase = r0 + (int64_t)warp * ROWS;
     if (rbase >= a.n) return;
-    float w[DIM][WN];
+    constexpr int NP = CW == 4 ? WN - 1 : 0;
+    Window<DIM, CW, NP> win;
 #pragma unroll
     for (int t = 0; t < WN; ++t) {
         const int64_t col = c0 + CW * lane + t;
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) w[d][t] = __ldg(a.pts + col * a.ld + d);
+        for (int d = 0; d < DIM; ++d) win.w[d][t] = __ldg(a.pts + col * a.ld + d);
     }
-    f2 W[DIM][6];
+    if constexpr (NP > 0) {
 #pragma unroll
-    for (int d = 0; d < DIM; ++d)
+        for (int d = 0; d < DIM; ++d)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) W[d][k] = pk2(w[d][k], w[d][k + 1]);
+            for (int k = 0; k < NP; ++k) win.W[d][k] = pk2(win.w[d][k], win.w[d][k + 1]);
+    }
     float pr[DIM];
     {
         const int64_t rr = rbase + (lane < ROWS ? lane : 0);
@@ -221,14 +179,8 @@ __device__ __forceinline__ void edm_tile_interior_x2(const EdmArgs &a, int64_t r
             const float p = __shfl_sync(0xffffffffu, pr[d], rr);
             P[d] = pk2(p, p);
         }
-        const int delta = (int)((0u - (uint32_t)s) & 3u);
-        float *dst = base + (s + (uint64_t)delta);
-        switch (delta) {
-            case 0: chunk_x2<DIM, 0>(P, W, dst); break;
-            case 1: chunk_x2<DIM, 1>(P, W, dst); break;
-            case 2: chunk_x2<DIM, 2>(P, W, dst); break;
-            default: chunk_x2<DIM, 3>(P, W, dst); break;
-        }
+        const int delta = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1));
+        chunk_phase_x2<DIM, CW, NP>(delta, P, win, base + (s + (uint64_t)delta));
         s += (uint64_t)(rbase + rr + 1);
     }
 }
@@ -273,10 +225,8 @@ __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, i
 template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-    if (RHO == 128 && bj + 1 < bi)
-        edm_tile_interior_x2<DIM>(a, r0, c0);
-    else if (RHO >= 128 && bj + 1 < bi)
-        edm_tile_interior<(RHO >= 128 ? RHO : 128), DIM>(a, r0, c0);
+    if (RHO >= 128 && bj + 1 < bi)
+        edm_tile_interior_x2<(RHO >= 128 ? RHO : 128), DIM>(a, r0, c0);
     else
         edm_tile_checked<RHO, DIM>(a, r0, c0);
 }
