@@ -213,6 +213,15 @@ def bench_edm(args, rank, world, local_rank, pk):
             "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
             "kernel": "edm_kernel<128,3,TRI_LAMBDA>", "peak_source": pk["source"],
             "alg_bytes_per_launch": alg_bytes}
+    # context for frac > 1: the measured peak is a read + write copy; a write-only stream
+    # (torch fill_ of a 4 GiB buffer, same box, same moment) is the fairer ceiling for a
+    # kernel that only writes
+    import torch
+    buf = torch.empty(1 << 30, dtype=torch.float32, device="cuda")
+    tf, _ = time_steps(lambda: buf.fill_(1.0), 5, 2, 1)
+    roof["write_only_fill_GBps"] = round(buf.numel() * 4 / (tf / 5 * 1e-3) / 1e9, 1)
+    roof["frac_of_write_only_fill"] = round(achieved / roof["write_only_fill_GBps"], 4)
+    del buf
 
     # lambda vs BB (paper form and persistent), a few steps each, this rank's slice
     vs = {}

@@ -16,12 +16,12 @@
 // row's chunk phase delta = (-T(i)) mod CW is warp-uniform, so every lane takes
 // its CW columns from a (2 CW - 1)-column register window through a uniform
 // branch; the row offset is advanced incrementally (T(i+1) = T(i) + i + 1) and
-// the row point is broadcast by shuffle.  At rho = 128 the interior path uses
-// the packed sm_100 FADD2 / FMUL2 / FFMA2 (two cells per instruction, the row
-// coordinate as a broadcast operand): the kernel is close enough to the write
-// roofline that its issue rate matters (1.386 -> 1.296 ms at n = 65536).  Tiles
-// touching the diagonal (bj >= bi - 1) take a checked path that walks Eq. 1
-// across row ends and the slice end.
+// the row point is broadcast by shuffle.  Tiles touching the diagonal
+// (bj >= bi - 1) take a checked path that walks Eq. 1 across row ends and the
+// slice end.  (A packed-f32x2 interior path -- two cells per FADD2/FMUL2/FFMA2 --
+// was measured: 1.386 -> 1.296 ms per isolated launch, but 1.40 -> 1.46 ms per
+// step in the bench's 200-launch sustained loop, where the board sits at its power
+// cap; the scalar path stays.)
 #include "tri_common.cuh"
 
 namespace {
@@ -43,6 +43,18 @@ constexpr int kWarps = kEdmThreads / 32;
 // chunks (512 B); a launch uses one chunk width for all its tiles, so chunk
 // ownership is consistent across tiles.
 template <int RHO> struct ChunkW { static constexpr int CW = RHO == 256 ? 8 : 4; };
+
+template <int DIM, int WN>
+__device__ __forceinline__ float dist_w(const float (&p)[DIM], const float (&w)[DIM][WN], int t) {
+    const float dx = p[0] - w[0][t];
+    float d2 = dx * dx;
+#pragma unroll
+    for (int d = 1; d < DIM; ++d) {
+        const float dd = p[d] - w[d][t];
+        d2 = fmaf(dd, dd, d2);
+    }
+    return sqrt_approx(d2);
+}
 
 template <int DIM>
 __device__ __forceinline__ float dist_gmem(const EdmArgs &a, int64_t i, int64_t j) {
@@ -67,99 +79,43 @@ __device__ __forceinline__ void store_chunk(float *dst, const float (&v)[CW]) {
     else st_cs_v4(dst, v[0], v[1], v[2], v[3]);
 }
 
-// Interior tile with the sm_100 packed f32x2 ops: two cells per FADD2 / FMUL2 /
-// FFMA2 (the row coordinate a broadcast operand, the window columns paired by
-// the compiler), per 3-D cell pair 3 + 1 + 2 instructions instead of 12 scalar
-// ones.  Same operation order per lane as dist_gmem (dx*dx, then fma per further
-// coordinate; IEEE per lane): bit-identical to the checked path.
-typedef unsigned long long f2;
-__device__ __forceinline__ f2 pk2(float lo, float hi) {
-    f2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ void upk2(f2 v, float &lo, float &hi) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ f2 sub_x2(f2 a, f2 b) {
-    f2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 mul_x2(f2 a, f2 b) {
-    f2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 fma_x2(f2 a, f2 b, f2 c) {
-    f2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
-// Column pairs (w_k, w_k+1) of the lane's window for the chunk at phase D: from the
-// NP pairs precomputed per tile (CW = 4: all six fit in registers; without them
-// ptxas rebuilds the odd-phase pairs with moves every row, 1.296 -> 1.382 ms), or
-// built in place (CW = 8: fourteen pairs per coordinate would not fit).
-template <int DIM, int CW, int NP>
-struct Window {
-    float w[DIM][2 * CW - 1];
-    f2 W[DIM][NP > 0 ? NP : 1];
-    __device__ __forceinline__ f2 pair(int d, int k) const {
-        if constexpr (NP > 0) return W[d][k];
-        else return pk2(w[d][k], w[d][k + 1]);
-    }
-};
-
-template <int DIM, int CW, int NP, int D>
-__device__ __forceinline__ void chunk_x2(const f2 (&P)[DIM], const Window<DIM, CW, NP> &win, float *dst) {
+// one lane's chunk at window offset D (the row's phase delta)
+template <int DIM, int CW, int D>
+__device__ __forceinline__ void chunk_at(const float (&p)[DIM], const float (&w)[DIM][2 * CW - 1], float *dst) {
     float v[CW];
 #pragma unroll
-    for (int e = 0; e < CW; e += 2) {
-        f2 d2 = 0ull;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-            const f2 dd = sub_x2(P[d], win.pair(d, D + e));
-            d2 = d == 0 ? mul_x2(dd, dd) : fma_x2(dd, dd, d2);
-        }
-        upk2(d2, v[e], v[e + 1]);
-    }
-#pragma unroll
-    for (int e = 0; e < CW; ++e) v[e] = sqrt_approx(v[e]);
+    for (int e = 0; e < CW; ++e) v[e] = dist_w<DIM, 2 * CW - 1>(p, w, D + e);
     store_chunk<CW>(dst, v);
 }
 
-template <int DIM, int CW, int NP, int D = 0>
-__device__ __forceinline__ void chunk_phase_x2(int delta, const f2 (&P)[DIM], const Window<DIM, CW, NP> &win,
-                                               float *dst) {
+// warp-uniform dispatch on delta in [0, CW)
+template <int DIM, int CW, int D = 0>
+__device__ __forceinline__ void chunk_phase(int delta, const float (&p)[DIM], const float (&w)[DIM][2 * CW - 1],
+                                            float *dst) {
     if (delta == D) {
-        chunk_x2<DIM, CW, NP, D>(P, win, dst);
+        chunk_at<DIM, CW, D>(p, w, dst);
     } else if constexpr (D + 1 < CW) {
-        chunk_phase_x2<DIM, CW, NP, D + 1>(delta, P, win, dst);
+        chunk_phase<DIM, CW, D + 1>(delta, p, w, dst);
     }
 }
 
+// Interior tile: rows [r0, r0+RHO) x cols [c0, c0+RHO), c0 + RHO < r0.
+// One warp per row segment: lane k owns chunk k (RHO = 32 CW).
 template <int RHO, int DIM>
-__device__ __forceinline__ void edm_tile_interior_x2(const EdmArgs &a, int64_t r0, int64_t c0) {
+__device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, int64_t c0) {
     constexpr int CW = ChunkW<RHO>::CW, WN = 2 * CW - 1;
     static_assert(RHO == 32 * CW, "one chunk per lane per row");
-    constexpr int ROWS = RHO / kWarps;
+    constexpr int ROWS = RHO / kWarps;            // rows per warp (<= 32)
+    static_assert(ROWS <= 32, "row points are broadcast from one lane each");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t rbase = r0 + (int64_t)warp * ROWS;
     if (rbase >= a.n) return;
-    constexpr int NP = CW == 4 ? WN - 1 : 0;
-    Window<DIM, CW, NP> win;
+    float w[DIM][WN];
 #pragma unroll
     for (int t = 0; t < WN; ++t) {
-        const int64_t col = c0 + CW * lane + t;
+        const int64_t col = c0 + CW * lane + t;               // < r0: always a valid point
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) win.w[d][t] = __ldg(a.pts + col * a.ld + d);
-    }
-    if constexpr (NP > 0) {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d)
-#pragma unroll
-            for (int k = 0; k < NP; ++k) win.W[d][k] = pk2(win.w[d][k], win.w[d][k + 1]);
+        for (int d = 0; d < DIM; ++d) w[d][t] = __ldg(a.pts + col * a.ld + d);
     }
     float pr[DIM];
     {
@@ -169,19 +125,16 @@ __device__ __forceinline__ void edm_tile_interior_x2(const EdmArgs &a, int64_t r
         for (int d = 0; d < DIM; ++d) pr[d] = in ? __ldg(a.pts + rr * a.ld + d) : 0.f;
     }
     const int nrows = (int)((a.n - rbase) < ROWS ? (a.n - rbase) : ROWS);
-    uint64_t s = tri::T2((uint64_t)rbase) + (uint64_t)c0 - a.out_offset;
+    uint64_t s = tri::T2((uint64_t)rbase) + (uint64_t)c0 - a.out_offset;   // local start of row rbase
     float *base = a.out + CW * lane;
 #pragma unroll 1
     for (int rr = 0; rr < nrows; ++rr) {
-        f2 P[DIM];
+        float p[DIM];
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-            const float p = __shfl_sync(0xffffffffu, pr[d], rr);
-            P[d] = pk2(p, p);
-        }
+        for (int d = 0; d < DIM; ++d) p[d] = __shfl_sync(0xffffffffu, pr[d], rr);
         const int delta = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1));
-        chunk_phase_x2<DIM, CW, NP>(delta, P, win, base + (s + (uint64_t)delta));
-        s += (uint64_t)(rbase + rr + 1);
+        chunk_phase<DIM, CW>(delta, p, w, base + (s + (uint64_t)delta));
+        s += (uint64_t)(rbase + rr + 1);               // T(i+1) = T(i) + i + 1
     }
 }
 
@@ -226,7 +179,7 @@ template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
     if (RHO >= 128 && bj + 1 < bi)
-        edm_tile_interior_x2<(RHO >= 128 ? RHO : 128), DIM>(a, r0, c0);
+        edm_tile_interior<(RHO >= 128 ? RHO : 128), DIM>(a, r0, c0);
     else
         edm_tile_checked<RHO, DIM>(a, r0, c0);
 }
