@@ -33,7 +33,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "triangular cells/sec and HBM GB/s (% of peak) at 1/2/4/8 B200 vs BB map"
 UNIT = "cells/s"
-EDM_N, EDM_RHO, EDM_STRAT = 65536, 128, "lambda"
+EDM_N, EDM_STRAT = 65536, "lambda"
+EDM_RHO = int(os.environ.get("TRI_EDM_RHO", "128"))          # tile edge (A/B hook; 128 is the measured best)
 
 
 def T(r):
