@@ -185,3 +185,47 @@ def test_triplet_partition_allreduce_matches_oracle(orc, world, n, rho):
     got = np.array(_run_tiles("triplet", world, n, rho))
     want = orc.triplet(inputs.points4(n, 42))
     assert np.allclose(got, want, rtol=1e-9, atol=1e-12 * np.abs(want).max())
+
+
+# ---------------------------------------------------------------- fused P2P halo address arithmetic
+@pytest.mark.parametrize("n,rho,world,k", [(2000, 128, 2, 4), (2000, 224, 3, 8), (5000, 128, 4, 16),
+                                           (1500, 224, 2, 1), (32768, 224, 8, 8)])
+def test_p2p_halo_addresses(n, rho, world, k):
+    """Host-only: P2PHalo buffers built on the CPU for every rank and linked by address.
+    Every cell a sender's kernel stores to a peer (include/tri.h: first k rows at
+    peer_above + slice offset, last k rows at peer_below + slice offset) must land
+    exactly where the receiver's next launch reads its halo (halo_above = rows
+    [R0 - k, R0) from T(R0 - k), halo_below = rows [R1, R1 + k) from T(R1)), in the
+    parity buffer that launch reads, and every peer pointer must be 16-byte aligned."""
+    from paper_1609_01490_b200 import dist as tdist
+    from paper_1609_01490_b200 import tri
+    maps = [tri.tri_map_init(n, rho, 1, g, world, 1) for g in range(world)]
+    bounds = [(m.row_begin, m.row_end) for m in maps]
+    hs = [tdist.P2PHalo(bounds, n, g, k, device="cpu", exchange=False) for g in range(world)]
+    for g, h in enumerate(hs):
+        R0, R1 = bounds[g]
+        up = tdist.owner(bounds, R0 - 1) if R0 > 0 else None
+        down = tdist.owner(bounds, R1) if R1 < n else None
+        h.link([t.data_ptr() for t in hs[up].below] if up is not None else None,
+               [t.data_ptr() for t in hs[down].above] if down is not None else None)
+    for e in range(3):
+        for g, h in enumerate(hs):
+            R0, R1 = bounds[g]
+            _, _, pa, pb = h.args(e)                  # what launch e of rank g stores into
+            for p in (pa, pb):
+                assert p is None or p % 16 == 0
+            if R0 > 0:                                # first k rows -> upper neighbour's below halo
+                up = tdist.owner(bounds, R0 - 1)
+                _, hb_next, _, _ = hs[up].args(e + 1)
+                for r in range(R0, min(R0 + k, R1)):
+                    for c in (0, r // 2, r):
+                        assert pa + (T(r) + c - T(R0)) == hb_next.data_ptr() + (T(r) + c - T(R0))
+                        assert 0 <= T(r) + c - T(R0) < hs[up].nb
+            if R1 < n:                                # last k rows -> lower neighbour's above halo
+                down = tdist.owner(bounds, R1)
+                ha_next, _, _, _ = hs[down].args(e + 1)
+                lo = max(R1 - k, 0)
+                for r in range(max(R1 - k, R0), R1):
+                    for c in (0, r // 2, r):
+                        assert pb + (T(r) + c - T(R0)) == ha_next.data_ptr() + (T(r) + c - T(lo))
+                        assert 0 <= T(r) + c - T(lo) < hs[down].na
