@@ -769,6 +769,15 @@ def test_ca_steps_p2p_emulated(orc, world, k, rho):
     assert np.array_equal(ca_steps_p2p_gpu(n, st, 3, k, "lambda", world, rho), orc.ca_run(n, st, 3 * k))
 
 
+@pytest.mark.parametrize("strategy", ["bb", "persist"])
+@pytest.mark.parametrize("world,k,rho", [(3, 8, 224), (2, 5, 128)])
+def test_ca_steps_p2p_strategies(orc, strategy, world, k, rho):
+    """The peer stores live in the shared store phase: BB and the persistent walk too."""
+    n = 1777
+    st = inputs.ca_state(n, 42)
+    assert np.array_equal(ca_steps_p2p_gpu(n, st, 2, k, strategy, world, rho), orc.ca_run(n, st, 2 * k))
+
+
 def test_ca_steps_p2p_single_rank_is_tri_ca_steps(orc):
     """world = 1: no peers, the result equals tri_ca_steps."""
     n = 1000
