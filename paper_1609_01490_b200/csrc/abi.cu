@@ -195,7 +195,8 @@ tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, i
 tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
                        unsigned long long *d_count, void *stream) {
     g_launches = 0;
-    if (bad_map(map) || bad_strategy(strategy) || !d_spheres || !d_count) return TRI_EINVAL;
+    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_LAMBDA_TC) || !d_spheres || !d_count)
+        return TRI_EINVAL;
     if (map->rho != 128 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
     if (((uintptr_t)d_spheres & 15u) != 0) return TRI_EINVAL;
     return launch_collide(*map, strategy, d_spheres, d_count, (cudaStream_t)stream);

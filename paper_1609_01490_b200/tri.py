@@ -22,7 +22,7 @@ TRI_LAMBDA_X, TRI_LAMBDA_N, TRI_LAMBDA_R = 3, 4, 5          # tri_dummy only (se
 TRI_SQRT_X, TRI_SQRT_N, TRI_SQRT_R = 1, 2, 3
 STRATEGIES = {"lambda": TRI_LAMBDA, "bb": TRI_BB, "persist": TRI_LAMBDA_PERSIST,
               "lambda_x": TRI_LAMBDA_X, "lambda_n": TRI_LAMBDA_N, "lambda_r": TRI_LAMBDA_R, "rb": 6,
-              "clc": TRI_LAMBDA_CLC}
+              "clc": TRI_LAMBDA_CLC, "tc": 8}
 TRI_RB = 6                                                   # tri_dummy / tri_edm, single rank
 
 c_u64, c_i64, c_i32, c_u32, c_vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p
