@@ -331,6 +331,13 @@ def bench_collide(rank, world, pk):
         t, _ = time_steps(step, 3, 1, world)
         res[st + "_ms"] = round(max_over_ranks(t, world) / 3, 4)
         res[st + "_count"] = int(cnt.item())
+    # the experimental tensor-core filter (TRI_LAMBDA_TC: 3xTF32 mma.sync), for comparison
+    def step_tc():
+        tri.tri_collide(m, "tc", s, cnt)
+        tdist.allreduce_count(cnt)
+    t, _ = time_steps(step_tc, 3, 1, world)
+    res["tc_ms"] = round(max_over_ranks(t, world) / 3, 4)
+    res["tc_count"] = int(cnt.item())
     pairs = n * (n - 1) // 2
     best = min(res["persist_ms"], res["lambda_ms"])
     res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
