@@ -20,8 +20,9 @@
 // (bj >= bi - 1) take a checked path that walks Eq. 1 across row ends and the
 // slice end.  (A packed-f32x2 interior path -- two cells per FADD2/FMUL2/FFMA2 --
 // was measured: 1.386 -> 1.296 ms per isolated launch, but 1.40 -> 1.46 ms per
-// step in the bench's 200-launch sustained loop, where the board sits at its power
-// cap; the scalar path stays.)
+// step in the bench's 200-launch sustained loop; the same store pattern with no
+// arithmetic at all is slower still there (1.47 ms): the packed layout's write
+// stream, not instruction issue, sets the pace, so the scalar path stays.)
 #include "tri_common.cuh"
 
 namespace {
