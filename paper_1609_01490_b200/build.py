@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtri.so")
 SOURCES = ["abi.cu", "map_eval.cu", "dummy.cu", "edm.cu", "collide.cu", "ca.cu", "triplet.cu", "rb.cu",
-           "collide1d.cu"]
+           "collide1d.cu", "collide_tc.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
