@@ -30,7 +30,7 @@ struct TcArgs {
     unsigned long long *count;
 };
 
-constexpr int kRho = 256, kThreads = 128, kCols = 256;
+constexpr int kRho = 256, kThreads = 128, kCols = 128;   // accumulator: 128 lanes x 128 fp32 columns
 constexpr float kKappaU = 1.0f / 32768.0f;     // 2^-15
 
 __device__ __forceinline__ float4 load_sph(const TcArgs &a, int64_t idx) {
@@ -172,16 +172,17 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
         const uint32_t tmem = sm.taddr;
         bool ok = true;
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < 4; ++pass) {
+            const int rh = pass >> 1, ch = pass & 1;        // row half, column half of the tile
             if (t == 0) {
-                const int g0 = pass * 16;                   // first 8-row group of this M = 128 pass
-                mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.yb[0]), 0u);
-                mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.ys[0]), 1u);
-                mma(tmem, smem_desc(&sm.xs[g0]), smem_desc(&sm.yb[0]), 1u);
+                const int g0 = rh * 16, h0 = ch * 16;       // first 8-row groups of the A and B halves
+                mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.yb[h0]), 0u);
+                mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.ys[h0]), 1u);
+                mma(tmem, smem_desc(&sm.xs[g0]), smem_desc(&sm.yb[h0]), 1u);
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     mb));
             }
-            ok = mbar_wait(mb, (uint32_t)pass) && ok;
+            ok = mbar_wait(mb, (uint32_t)(pass & 1)) && ok;
             asm volatile("tcgen05.fence::after_thread_sync;");
             // epilogue: thread t = accumulator lane t = row 128 pass + t; 8 groups of 32 columns
             uint32_t flags = 0;
@@ -205,13 +206,13 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
                 flags |= (o >> 31) << cg;
             }
             // rare: the exact predicate on this row's flagged 32-column groups
-            const float4 p = prow[pass];
+            const float4 p = prow[rh];
 #pragma unroll 1
             while (flags) {
                 const int cg = __ffs(flags) - 1;
                 flags &= flags - 1;
 #pragma unroll 4
-                for (int j = 32 * cg; j < 32 * cg + 32; ++j) cnt += hit(p, sm.col[j]);
+                for (int j = 128 * ch + 32 * cg; j < 128 * ch + 32 * cg + 32; ++j) cnt += hit(p, sm.col[j]);
             }
             // every lane's loads are done before pass 1 overwrites the accumulator
             asm volatile("tcgen05.fence::before_thread_sync;");
