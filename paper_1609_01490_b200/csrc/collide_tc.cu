@@ -200,9 +200,10 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
                       "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                     : "r"(ta));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                uint32_t o = 0;
+                uint32_t o = 0;                             // OR of 32 sign bits, 3-input LOP3s
 #pragma unroll
-                for (int e = 0; e < 32; ++e) o |= v[e];
+                for (int e = 0; e < 32; e += 2)
+                    asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(o), "r"(v[e]), "r"(v[e + 1]));
                 flags |= (o >> 31) << cg;
             }
             // rare: the exact predicate on this row's flagged 32-column groups
