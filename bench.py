@@ -47,9 +47,10 @@ def peaks():
         with open(p) as f:
             d = json.load(f)
         return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
-                "source": "measured (MEASURED_PEAKS.json)"}
+                "bf16_tflops": float(d.get("bf16_tflops", 2250.0)), "source": "measured (MEASURED_PEAKS.json)"}
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "bf16_tflops": 2250.0,
+                "source": "fallback (B200_PROFILING.md)"}
 
 
 def ncu_traffic(name):
@@ -339,18 +340,31 @@ def bench_collide(rank, world, pk):
     res["tc_ms"] = round(max_over_ranks(t, world) / 3, 4)
     res["tc_count"] = int(cnt.item())
     pairs = n * (n - 1) // 2
-    best = min(res["persist_ms"], res["lambda_ms"])
+    simt = min(res["persist_ms"], res["lambda_ms"])
+    best = min(simt, res["tc_ms"]) if res["tc_count"] == res["lambda_count"] else simt
+    res["best"] = "tc" if best == res.get("tc_ms") else ("lambda" if best == res["lambda_ms"] else "persist")
     res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
     res["I_persist"] = round(res["bb_ms"] / res["persist_ms"], 4)
-    # FP32-pipe roofline: the hot loop's 5 fma-pipe ops per pair (the 4-D dot-product
-    # filter: 4 FFMA + 1 FADD, packed f32x2) on 128 lanes/SM; the exact 9-op predicate
-    # runs only on flagged (row, column) pairs (~7e-6 of them)
-    ops = 5.0 * pairs / world
+    res["I_tc"] = round(res["bb_ms"] / res["tc_ms"], 4)
+    # SIMT roofline: the hot loop's 5 fma-pipe ops per pair (the 4-D dot-product filter:
+    # 4 FFMA + 1 FADD, packed f32x2) on 128 lanes/SM; the exact 9-op predicate runs only
+    # on flagged (row, column) pairs (~7e-6 of them)
     peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
-    ach = ops / (best * 1e-3) / 1e12
-    res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "TFLOP/s (fp32 ops)",
-                       "frac": round(ach / peak, 4), "ops_per_pair": 5,
-                       "note": "filter ops; the exact predicate (9 ops) runs on flagged pairs only"}
+    ach = 5.0 * pairs / world / (simt * 1e-3) / 1e12
+    simt_roof = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "TFLOP/s (fp32 ops)",
+                 "frac": round(ach / peak, 4), "ops_per_pair": 5, "kernel": "collide_kernel<256> (SIMT filter)",
+                 "note": "filter ops; the exact predicate (9 ops) runs on flagged pairs only"}
+    # tensor roofline of the tcgen05 filter: 3 kind::tf32 MMAs (3xTF32 split) with K = 8
+    # per pair = 48 executed TF32 flops per pair, against the TF32 dense peak (the measured
+    # bf16 cuBLAS peak x the nominal tf32 : bf16 ratio 1 : 2)
+    tpeak = pk["bf16_tflops"] / 2.0
+    tach = 48.0 * pairs / world / (res["tc_ms"] * 1e-3) / 1e12
+    tc_roof = {"bound": "tensor", "achieved": round(tach, 1), "peak": round(tpeak, 1), "unit": "TFLOP/s (tf32)",
+               "frac": round(tach / tpeak, 4), "flops_per_pair": 48, "kernel": "collide_tc_kernel (tcgen05)",
+               "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (nominal tf32 rate)"}
+    res["roofline"] = tc_roof if res["best"] == "tc" else simt_roof
+    res["roofline_simt"] = simt_roof
+    res["roofline_tc"] = tc_roof
     return {"config": "collision count, n=200000 spheres, r~U[0,0.01)", "metric": "pair tests/s",
             "value": pairs / (best * 1e-3), **res}
 
