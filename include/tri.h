@@ -52,8 +52,8 @@ typedef enum {
 
 enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2, TRI_LAMBDA_CLC = 7 };
 /* tri_collide only, rho = 256: the TRI_LAMBDA grid with the filter gap evaluated on the
- * tensor cores (3xTF32 mma.sync contraction, csrc/collide.cu "TRI_LAMBDA_TC"); the count
- * is the same exact fixed-order predicate. */
+ * 5th-generation tensor cores (3xTF32 tcgen05.mma into TMEM, csrc/collide_tc.cu); the
+ * count is the same exact fixed-order predicate (reading Q9). */
 enum { TRI_LAMBDA_TC = 8 };
 /* The paper's square-root variants of Eq. 4 (section 4.1), used WITHOUT
  * the integer correction: lambda_X = IEEE sqrtf, lambda_N = 0x5f3759df seed + 3

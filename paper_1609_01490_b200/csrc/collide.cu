@@ -225,151 +225,6 @@ __global__ void __launch_bounds__(RHO / rows_per_thread<RHO>()) collide_kernel(C
     flush_count<RHO / rows_per_thread<RHO>()>(cnt, a.count);
 }
 
-// ============================================================================
-// TRI_LAMBDA_TC (rho = 256): the filter gap as a tensor-core contraction.
-// g_ij = A'_i + A'_j - 2 (x_i x_j + y_i y_j + z_i z_j + r_i r_j) = X_i . Y_j with
-//   X_i = (x, y, z, r, A'_i, 1),  Y_j = (-2x, -2y, -2z, -2r, 1, A'_j),
-// each split into TF32 big + small parts (3xTF32: X_big.Y_big + X_big.Y_small +
-// X_small.Y_big, K = 3 x 8 with 6 of every 8 used), mma.sync m16n8k8 (fp32
-// accumulate).  The omitted small.small term and the accumulator rounding are
-// <= ~2^-17 (M_i + M_j); A' here carries kappa_tc u M with kappa_tc u = 2^-15, so
-// every pair the fixed-order predicate counts still has g < 0.  A warp owns 32
-// rows x 256 columns; the sign bits of its accumulators are OR-ed per 32-column
-// block and a flagged block is recounted with the exact predicate.  Diagonal
-// tiles take the SIMT path.
-namespace tc {
-
-constexpr float kKappaU = 1.0f / 32768.0f;      // 2^-15
-
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ void split(float x, uint32_t &big, uint32_t &small) {
-    big = to_tf32(x);
-    small = to_tf32(x - __uint_as_float(big));
-}
-__device__ __forceinline__ float a_tc(const float4 c) {
-    const float q = fmaf(c.z, c.z, fmaf(c.y, c.y, c.x * c.x));
-    const float w = c.w * c.w;
-    return fmaf(-kKappaU, q + w, q - w);
-}
-// component k (0..7) of X_i / Y_j
-__device__ __forceinline__ float xk(const float4 c, float A, int k) {
-    return k == 0 ? c.x : k == 1 ? c.y : k == 2 ? c.z : k == 3 ? c.w : k == 4 ? A : k == 5 ? 1.f : 0.f;
-}
-__device__ __forceinline__ float yk(const float4 c, float A, int k) {
-    return k == 0 ? -2.f * c.x : k == 1 ? -2.f * c.y : k == 2 ? -2.f * c.z : k == 3 ? -2.f * c.w
-         : k == 4 ? 1.f : k == 5 ? A : 0.f;
-}
-
-__device__ __forceinline__ void mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};"
-                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-struct Smem {
-    uint2 yb[32][3][32];      // B fragments: [n-tile][k-step][lane] = (b0, b1)
-    float4 col[256];          // column spheres (exact recount)
-};
-
-__device__ __forceinline__ uint32_t tile(const CollideArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
-    constexpr int RHO = 256;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int g = lane >> 2, q4 = lane & 3;
-    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-    // stage columns: sphere, then the lane-ordered B fragments of the 3 k-steps
-    sm.col[t] = load_sphere(a, c0 + t);
-    __syncthreads();
-    if (bi == bj) {                                         // diagonal tile: strict j < i, exact
-        const float4 p = load_sphere(a, r0 + t);
-        uint32_t c1 = 0;
-#pragma unroll 4
-        for (int c = 0; c < t; ++c) {
-            const float4 v = sm.col[c];
-            c1 += hit(p, v.x, v.y, v.z, v.w);
-        }
-        return c1;
-    }
-#pragma unroll
-    for (int e = 0; e < 12; ++e) {                          // 32 x 3 x 32 entries / 256 threads
-        const int idx = t + 256 * e;
-        const int L = idx & 31, ks = (idx >> 5) % 3, nt = idx / 96;
-        const int gg = L >> 2, tt = L & 3;
-        const float4 c = sm.col[8 * nt + gg];
-        const float A = a_tc(c);
-        uint32_t bb0, bs0, bb1, bs1;
-        split(yk(c, A, tt), bb0, bs0);
-        split(yk(c, A, tt + 4), bb1, bs1);
-        // k-step 0: X_big . Y_big, 1: X_big . Y_small, 2: X_small . Y_big
-        sm.yb[nt][ks][L] = ks == 1 ? make_uint2(bs0, bs1) : make_uint2(bb0, bb1);
-    }
-    // A fragments of the warp's 32 rows (2 m-tiles)
-    uint32_t af[2][3][4];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-        const float4 p0 = load_sphere(a, r0 + 32 * warp + 16 * mt + g);
-        const float4 p1 = load_sphere(a, r0 + 32 * warp + 16 * mt + g + 8);
-        const float A0 = a_tc(p0), A1 = a_tc(p1);
-        uint32_t b00, s00, b10, s10, b01, s01, b11, s11;
-        split(xk(p0, A0, q4), b00, s00);
-        split(xk(p1, A1, q4), b10, s10);
-        split(xk(p0, A0, q4 + 4), b01, s01);
-        split(xk(p1, A1, q4 + 4), b11, s11);
-        const uint32_t big[4] = {b00, b10, b01, b11}, sml[4] = {s00, s10, s01, s11};
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            af[mt][0][r] = big[r];
-            af[mt][1][r] = big[r];
-            af[mt][2][r] = sml[r];
-        }
-    }
-    const float4 myrow = load_sphere(a, r0 + 32 * warp + lane);  // exact recount: lane = row
-    __syncthreads();
-    uint32_t cnt = 0;
-#pragma unroll 1
-    for (int cb = 0; cb < 32; cb += 4) {                    // 4 n-tiles = 32 columns per flag block
-        uint32_t flag = 0;
-#pragma unroll
-        for (int nt = cb; nt < cb + 4; ++nt) {
-            float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-            for (int ks = 0; ks < 3; ++ks) {
-                const uint2 b = sm.yb[nt][ks][lane];
-                mma(d[0], af[0][ks], b.x, b.y);
-                mma(d[1], af[1][ks], b.x, b.y);
-            }
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-                flag |= __float_as_uint(d[mt][0]) | __float_as_uint(d[mt][1]) | __float_as_uint(d[mt][2]) |
-                        __float_as_uint(d[mt][3]);
-        }
-        if (__any_sync(0xffffffffu, (int32_t)flag < 0)) {
-            // rare: the warp's 32 rows x these 32 columns with the exact predicate
-#pragma unroll 1
-            for (int c = 8 * cb; c < 8 * cb + 32; ++c) {
-                const float4 v = sm.col[c];
-                cnt += hit(myrow, v.x, v.y, v.z, v.w);
-            }
-        }
-    }
-    __syncthreads();
-    return cnt;
-}
-
-__global__ void __launch_bounds__(256) collide_tc_kernel(CollideArgs a) {
-    __shared__ __align__(16) Smem sm;
-    const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
-    if (w >= a.omega_end) return;
-    uint32_t bi, bj;
-    tri::lambda_map(w, bi, bj);
-    flush_count<256>(tile(a, bi, bj, sm), a.count);
-}
-
-}  // namespace tc
 
 template <int RHO>
 tri_status launch_r(const tri_map_t &m, int strategy, CollideArgs a, cudaStream_t st) {
