@@ -2,7 +2,7 @@
 # Run ON the GPU box: compute-sanitizer over the small-size GPU parity tests (the
 # full-size and exhaustive ones would take hours under the tools) -> gpurun_out/sanitizer.txt
 OUT=gpurun_out/sanitizer.txt; mkdir -p gpurun_out; : > $OUT
-SMALL="(map_matches_enumeration or dummy_packed or dummy_ranks or edm_small or edm_dims or edm_ranks or collide_small or collide_quantized or ca_small or ca_ranks or ca_ignores or ca_steps_single or ca_steps_deep or ca_steps_ignores or ca_steps_rho224 or ca_steps_p2p_emulated or ca_steps_p2p_single or knife_edge or triplet_small or triplet_ranks or collide1d or tet_lut_map_matches or abi_rejects)"
+SMALL="(map_matches_enumeration or dummy_packed or dummy_ranks or edm_small or edm_dims or edm_ranks or collide_small or collide_quantized or ca_small or ca_ranks or ca_ignores or ca_steps_single or ca_steps_deep or ca_steps_ignores or ca_steps_rho224 or ca_steps_p2p_emulated or ca_steps_p2p_single or knife_edge or collide_tc_small or triplet_small or triplet_ranks or collide1d or tet_lut_map_matches or abi_rejects)"
 run() { tool=$1; sel=$2; echo "== compute-sanitizer --tool $tool, pytest -k \"$sel\"" >> $OUT
   compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
     python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "$sel" 2>&1 | \
