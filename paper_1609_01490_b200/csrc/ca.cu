@@ -2,8 +2,9 @@
 // (P:79-80 names cellular automata on triangular domains, citing Conway's
 // Life; cells outside the triangle are dead -- DESIGN.md reading Q11).
 // State: u8 {0,1} in the packed Eq. 1 layout.  Three kernels:
-//   rho = 128: multi::ca_multi_kernel -- k generations per launch on a
-//              register-resident bitmap (tri_ca_steps; tri_ca_step is k = 1);
+//   rho = 128, 224: multi::ca_multi_kernel -- k generations per launch on a
+//              register-resident bitmap (tri_ca_steps; tri_ca_step is k = 1;
+//              tri_ca_steps_p2p also stores the halo rows into peer memory);
 //   rho = 256: bits::ca_bits_kernel -- one generation, shared-memory bitmaps;
 //   rho = 512: ca_kernel -- one generation, byte SWAR (described next).
 //
@@ -603,7 +604,7 @@ tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
 
 // ============================================================================
 // k generations per launch (temporal blocking with deep halos);
-// also tri_ca_step at rho = 128 (k = 1).  rho = 128 tiles; the CTA loads rows
+// also tri_ca_step at rho = 128 / 224 (k = 1).  rho x rho tiles; the CTA loads rows
 // [r0-k, r0+rho+k) x columns [c0-k, c0+rho+k), packs them to bitmaps, runs k
 // generations with the bitmap in registers -- re-masking the triangle after
 // each one -- and writes only its own row segments [c0, min(c0+rho, i+1)): aligned chunks
