@@ -1,4 +1,4 @@
-// collide_tc.cu -- TRI_LAMBDA_TC for tri_collide (rho = 256): the collision
+// collide_tc.cu -- TRI_LAMBDA_TC for tri_collide (rho = 256 or 512): the collision
 // filter gap of collide.cu evaluated on the 5th-generation tensor cores.
 //
 //   g_ij = A'_i + A'_j - 2 (x_i x_j + y_i y_j + z_i z_j + r_i r_j) = X_i . Y_j,
@@ -14,8 +14,10 @@
 // the epilogue ORs the sign bits of each row's 32-column groups and recounts a
 // flagged group with the exact scalar predicate, so the count is exact.
 //
-// CTA = 128 threads (4 warps) per lambda tile; the tile's 256 rows are two
-// M = 128 passes over one 128 x 256 fp32 accumulator (256 TMEM columns).
+// CTA = 128 threads (4 warps) per lambda tile; the tile is (rho/128)^2 blocks of
+// 128 x 128, each one M = 128, N = 128 accumulator pass over 128 TMEM columns
+// (rho = 512: 16 passes per CTA, 4x the pairs per TMEM allocation and barrier
+// set-up of rho = 256: 2.42 vs 2.83 ms).
 // Operands: K-major, no swizzle, canonical 8-row x 16-byte core matrices
 // (LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups).
 // Diagonal tiles (strict j < i) are counted with the scalar predicate.
@@ -30,7 +32,7 @@ struct TcArgs {
     unsigned long long *count;
 };
 
-constexpr int kRho = 256, kThreads = 128, kCols = 128;   // accumulator: 128 lanes x 128 fp32 columns
+constexpr int kThreads = 128, kCols = 128;   // accumulator: 128 lanes x 128 fp32 columns
 constexpr float kKappaU = 1.0f / 32768.0f;     // 2^-15
 
 __device__ __forceinline__ float4 load_sph(const TcArgs &a, int64_t idx) {
@@ -59,6 +61,7 @@ __device__ __forceinline__ uint32_t tf32(float x) {
     return r;
 }
 
+template <int kRho>
 struct __align__(128) Smem {
     // operand rows: 32 B (K = 8 tf32) each, in the canonical core-matrix order
     uint32_t xb[kRho / 8][2][8][4], xs[kRho / 8][2][8][4];     // rows (A): big / small
@@ -114,8 +117,10 @@ __device__ __forceinline__ bool mbar_wait(uint32_t mb, uint32_t parity) {
     return false;
 }
 
+template <int kRho>
 __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
-    __shared__ Smem sm;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    Smem<kRho> &sm = *reinterpret_cast<Smem<kRho> *>(dsm);
     const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
     if (w >= a.omega_end) return;
     uint32_t bi, bj;
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
 
     // columns: spheres for the recount, Y big / small operand rows
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kRho / kThreads; ++h) {
         const int j = t + kThreads * h;
         const float4 c = load_sph(a, c0 + j);
         sm.col[j] = c;
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
     if (bi == bj) {                                      // diagonal tile: strict j < i, scalar exact
         __syncthreads();
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kRho / kThreads; ++h) {
             const int i = t + kThreads * h;
             const float4 p = load_sph(a, r0 + i);
 #pragma unroll 4
@@ -144,9 +149,9 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
         }
     } else {
         // rows: X big / small operand rows (all 256; pass p uses rows 128 p ..)
-        float4 prow[2];
+        float4 prow[kRho / kThreads];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kRho / kThreads; ++h) {
             const int i = t + kThreads * h;
             const float4 p = load_sph(a, r0 + i);
             prow[h] = p;
@@ -172,8 +177,8 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
         const uint32_t tmem = sm.taddr;
         bool ok = true;
 #pragma unroll 1
-        for (int pass = 0; pass < 4; ++pass) {
-            const int rh = pass >> 1, ch = pass & 1;        // row half, column half of the tile
+        for (int pass = 0; pass < (kRho / 128) * (kRho / 128); ++pass) {
+            const int rh = pass / (kRho / 128), ch = pass % (kRho / 128);   // 128-row, 128-column block
             if (t == 0) {
                 const int g0 = rh * 16, h0 = ch * 16;       // first 8-row groups of the A and B halves
                 mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.yb[h0]), 0u);
@@ -234,8 +239,15 @@ __global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
 
 namespace tri {
 
+template <int kRho>
+static void launch_rho(TcArgs a, uint64_t nb, cudaStream_t st) {
+    const int smem = (int)sizeof(Smem<kRho>);
+    cudaFuncSetAttribute(collide_tc_kernel<kRho>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    collide_tc_kernel<kRho><<<tile_grid(nb), kThreads, smem, st>>>(a);
+}
+
 tri_status launch_collide_tc(const tri_map_t &m, const float *sph, unsigned long long *count, cudaStream_t st) {
-    if (m.rho != kRho) return TRI_EINVAL;
+    if (m.rho != 256 && m.rho != 512) return TRI_EINVAL;
     TcArgs a;
     a.sph = (const float4 *)sph;
     a.n = m.n;
@@ -245,7 +257,8 @@ tri_status launch_collide_tc(const tri_map_t &m, const float *sph, unsigned long
     if (cudaMemsetAsync(count, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
     const uint64_t nb = a.omega_end - a.omega_begin;
     if (!nb) return TRI_OK;
-    collide_tc_kernel<<<tile_grid(nb), kThreads, 0, st>>>(a);
+    if (m.rho == 512) launch_rho<512>(a, nb, st);
+    else launch_rho<256>(a, nb, st);
     note_launches(1);
     return cuda_status();
 }

@@ -314,22 +314,24 @@ def test_collide_knife_edge_pairs(orc, offset, scale):
             assert cnt.item() == ref, (rho, strategy)
 
 
+@pytest.mark.parametrize("rho", [256, 512])
 @pytest.mark.parametrize("n,seed,rmax", [(1, 7, 0.1), (300, 42, 0.2), (1000, 42, 0.05), (5000, 7, 0.02),
                                          (777, 42, 0.08)])
-def test_collide_tc_small(orc, n, seed, rmax):
-    """TRI_LAMBDA_TC: the filter gap on the tensor cores (3xTF32 mma.sync), exact count."""
+def test_collide_tc_small(orc, n, seed, rmax, rho):
+    """TRI_LAMBDA_TC: the filter gap on the tensor cores (3xTF32 tcgen05), exact count."""
     s = inputs.spheres(n, seed, rmax)
-    m = tri.tri_map_init(n, 256)
+    m = tri.tri_map_init(n, rho)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     tri.tri_collide(m, "tc", torch.from_numpy(s).cuda(), cnt)
     sync()
     assert cnt.item() == orc.collide(s)
 
 
+@pytest.mark.parametrize("rho", [256, 512])
 @pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (0.5, 1.0), (100.0, 1.0), (-1000.0, 10.0), (0.0, 1e-3)])
-def test_collide_tc_knife_edge(orc, offset, scale):
+def test_collide_tc_knife_edge(orc, offset, scale, rho):
     s = _near_touching(8192, 11, offset, scale)
-    m = tri.tri_map_init(len(s), 256)
+    m = tri.tri_map_init(len(s), rho)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     tri.tri_collide(m, "tc", torch.from_numpy(s).cuda(), cnt)
     sync()
@@ -340,8 +342,8 @@ def test_collide_tc_full_size_rank_slice(orc):
     n = 200000
     s = inputs.spheres(n, 42)
     d = torch.from_numpy(s).cuda()
-    for g in (0, 40):
-        m = tri.tri_map_init(n, 256, 1, g, 256, 1)          # snapped: the slice is whole rows
+    for g, rho in ((0, 256), (40, 256), (0, 512), (20, 512)):
+        m = tri.tri_map_init(n, rho, 1, g, 128 if rho == 512 else 256, 1)   # snapped: whole rows
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         tri.tri_collide(m, "tc", d, cnt)
         sync()
