@@ -350,6 +350,23 @@ def test_collide_tc_full_size_rank_slice(orc):
         assert cnt.item() == orc.collide(s, m.row_begin, m.row_end)
 
 
+@pytest.mark.parametrize("rho", [256, 512])
+def test_collide_tc_plain_ranks(orc, rho):
+    """tcgen05 filter on plain (unsnapped) omega ranges of 3 ranks: the partial counts sum
+    to the oracle's total (11-bit-quantised spheres: every fp32 op exact)."""
+    n = 20000
+    s = inputs.spheres_quantized(n, 42, 11, 0.01)
+    d = torch.from_numpy(s).cuda()
+    tot = 0
+    for g in range(3):
+        m = tri.tri_map_init(n, rho, 1, g, 3, 0)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tri.tri_collide(m, "tc", d, cnt)
+        sync()
+        tot += cnt.item()
+    assert tot == orc.collide(s)
+
+
 def test_collide_full_size_rank_slice(orc):
     """BASELINE configs[2] (n = 200000): one 64-way snapped rank slice vs the oracle rows."""
     n = 200000
