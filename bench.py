@@ -333,7 +333,7 @@ def bench_collide(rank, world, pk):
         res[st + "_ms"] = round(max_over_ranks(t, world) / 3, 4)
         res[st + "_count"] = int(cnt.item())
     # the experimental tensor-core filter (TRI_LAMBDA_TC: 3xTF32 mma.sync), for comparison
-    m_tc = tri.tri_map_init(n, 512, 1, rank, world, 0)          # the tcgen05 kernel's best tile edge
+    m_tc = tri.tri_map_init(n, 384, 1, rank, world, 0)          # the tcgen05 kernel's best tile edge
     def step_tc():
         tri.tri_collide(m_tc, "tc", s, cnt)
         tdist.allreduce_count(cnt)

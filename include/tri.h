@@ -51,7 +51,8 @@ typedef enum {
 } tri_status;
 
 enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2, TRI_LAMBDA_CLC = 7 };
-/* tri_collide only, rho = 256 or 512: the TRI_LAMBDA grid with the filter gap evaluated on the
+/* tri_collide only, rho = 256, 384 or 512 (384: this strategy only): the TRI_LAMBDA grid with
+ * the filter gap evaluated on the
  * 5th-generation tensor cores (3xTF32 tcgen05.mma into TMEM, csrc/collide_tc.cu); the
  * count is the same exact fixed-order predicate (reading Q9). */
 enum { TRI_LAMBDA_TC = 8 };

@@ -197,7 +197,8 @@ tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_sp
     g_launches = 0;
     if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_LAMBDA_TC) || !d_spheres || !d_count)
         return TRI_EINVAL;
-    if (map->rho != 128 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
+    if (map->rho != 128 && map->rho != 256 && map->rho != 384 && map->rho != 512) return TRI_EINVAL;
+    if (map->rho == 384 && strategy != TRI_LAMBDA_TC) return TRI_EINVAL;      // tcgen05 tile edge only
     if (((uintptr_t)d_spheres & 15u) != 0) return TRI_EINVAL;
     return launch_collide(*map, strategy, d_spheres, d_count, (cudaStream_t)stream);
 }

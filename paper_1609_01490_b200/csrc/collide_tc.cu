@@ -1,4 +1,4 @@
-// collide_tc.cu -- TRI_LAMBDA_TC for tri_collide (rho = 256 or 512): the collision
+// collide_tc.cu -- TRI_LAMBDA_TC for tri_collide (rho = 256, 384 or 512): the collision
 // filter gap of collide.cu evaluated on the 5th-generation tensor cores.
 //
 //   g_ij = A'_i + A'_j - 2 (x_i x_j + y_i y_j + z_i z_j + r_i r_j) = X_i . Y_j,
@@ -16,8 +16,9 @@
 //
 // CTA = 128 threads (4 warps) per lambda tile; the tile is (rho/128)^2 blocks of
 // 128 x 128, each one M = 128, N = 128 accumulator pass over 128 TMEM columns
-// (rho = 512: 16 passes per CTA, 4x the pairs per TMEM allocation and barrier
-// set-up of rho = 256: 2.42 vs 2.83 ms).
+// (larger tiles amortise the TMEM allocation and barrier set-up: rho = 256 2.83 ms,
+// 512 2.41 ms (74 KB smem: 3 CTAs per SM), 384 2.24 ms (55 KB: 4 CTAs, as many as
+// can hold their 128 TMEM columns at once)).
 // Operands: K-major, no swizzle, canonical 8-row x 16-byte core matrices
 // (LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups).
 // Diagonal tiles (strict j < i) are counted with the scalar predicate.
@@ -247,7 +248,7 @@ static void launch_rho(TcArgs a, uint64_t nb, cudaStream_t st) {
 }
 
 tri_status launch_collide_tc(const tri_map_t &m, const float *sph, unsigned long long *count, cudaStream_t st) {
-    if (m.rho != 256 && m.rho != 512) return TRI_EINVAL;
+    if (m.rho != 256 && m.rho != 384 && m.rho != 512) return TRI_EINVAL;
     TcArgs a;
     a.sph = (const float4 *)sph;
     a.n = m.n;
@@ -258,6 +259,7 @@ tri_status launch_collide_tc(const tri_map_t &m, const float *sph, unsigned long
     const uint64_t nb = a.omega_end - a.omega_begin;
     if (!nb) return TRI_OK;
     if (m.rho == 512) launch_rho<512>(a, nb, st);
+    else if (m.rho == 384) launch_rho<384>(a, nb, st);
     else launch_rho<256>(a, nb, st);
     note_launches(1);
     return cuda_status();

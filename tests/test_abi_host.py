@@ -143,6 +143,16 @@ def test_ca_steps_p2p_validation(L):
     assert L.tri_ipc_close(None) == tri.TRI_EINVAL
 
 
+def test_collide_rho384_is_tc_only(L):
+    """rho = 384 is a tile edge of the tcgen05 collision kernel only: the SIMT strategies
+    reject it with EINVAL before any launch (fake device pointers)."""
+    import ctypes
+    m = tri.tri_map_init(1000, 384)
+    for strat in (tri.TRI_LAMBDA, tri.TRI_BB, tri.TRI_LAMBDA_PERSIST):
+        assert L.tri_collide(ctypes.byref(m), strat, ctypes.c_void_p(1 << 20), ctypes.c_void_p(2 << 20),
+                             None) == tri.TRI_EINVAL
+
+
 def test_host_lambda_vs_oracle(L, orc):
     rng = random.Random(5)
     ws = list(range(0, 5000)) + [rng.randrange(0, 2**40) for _ in range(3000)]

@@ -11,7 +11,7 @@ cap() { name=$1; shift; ncu --set full --clock-control none --import-source on -
         python tools/run_one.py "$@" --reps 1 > gpurun_out/$name.log 2>&1; }
 cap edm edm --rho 128 --strategy lambda
 cap collide collide --rho 256 --strategy lambda
-cap collide_tc collide --rho 512 --strategy tc
+cap collide_tc collide --rho 384 --strategy tc
 cap collide1d collide1d --strategy lambda
 cap ca ca --rho 128 --strategy lambda
 cap ca_multi ca_steps --rho 224 --k 8 --strategy lambda
