@@ -454,7 +454,11 @@ int orc_triplet_total(int64_t n, const float *pts, double nu, double *total)
 /*   x = 1/4 + 2 w (fp32), s = sqrt(x) by the variant, i = floor(s - 1/2)      */
 /*   variant 1 (lambda_X): s = sqrtf(x) */
 /*   variant 2 (lambda_N): y0 = bits(0x5f3759df - (bits(x) >> 1)), three      */
-/*     Newton steps y = y (1.5 - (x/2) y^2), s = x y + 1e-4 */
+/*     Newton steps y = y (1.5 - ((x/2) y) y), s = x y + 1e-4 */
+/*     -- the Carmack / Lomont code the passage cites evaluates its step as    */
+/*     y * (threehalfs - (x2 * y * y)), C's left-to-right (x2 * y) * y; that   */
+/*     operation order is kept (it decides the first failing omega,            */
+/*     tests/golden/sqrt_variants.txt; reading Q5b).                 */
 /* every operation IEEE fp32 round-to-nearest in this order (no contraction).  */
 /* lambda_R (hardware rsqrt) has no CPU definition: parity unpinned.           */
 /* The variant is correct at w iff T(i) <= w < T(i+1) (Eq. 3).      */
@@ -474,8 +478,8 @@ static uint32_t variant_row(uint64_t w, int variant)
         bits = 0x5f3759df - (bits >> 1);
         memcpy(&y, &bits, 4);
         for (int it = 0; it < 3; ++it) {
-            float yy = y * y;
-            float t = xh * yy;
+            float xy2 = xh * y;
+            float t = xy2 * y;
             float u = 1.5f - t;
             y = y * u;
         }

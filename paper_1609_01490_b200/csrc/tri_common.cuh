@@ -77,11 +77,12 @@ TRI_HD float sqrt_variant(float x, int variant) {
 #ifdef __CUDA_ARCH__
     if (variant == TRI_SQRT_X) return __fsqrt_rn(x);
     if (variant == TRI_SQRT_R) return __fadd_rn(__fmul_rn(x, rsqrtf(x)), 1e-4f);
-    // lambda_N: Carmack / Lomont reciprocal square root, three Newton steps
+    // lambda_N: Carmack / Lomont reciprocal square root, three Newton steps in
+    // the cited code's order y * (1.5 - (x2 * y) * y)
     const float xh = __fmul_rn(0.5f, x);
     float y = __int_as_float(0x5f3759df - (__float_as_int(x) >> 1));
 #pragma unroll
-    for (int it = 0; it < 3; ++it) y = __fmul_rn(y, __fsub_rn(1.5f, __fmul_rn(xh, __fmul_rn(y, y))));
+    for (int it = 0; it < 3; ++it) y = __fmul_rn(y, __fsub_rn(1.5f, __fmul_rn(__fmul_rn(xh, y), y)));
     return __fadd_rn(__fmul_rn(x, y), 1e-4f);
 #else
     (void)variant;

@@ -104,6 +104,9 @@ def test_sqrt_variant_scan_matches_oracle(orc, variant, count):
     sync()
     nf, fw = orc.variant_scan(variant, 0, count)
     assert fail.item() == nf and first.item() == fw
+    from conftest import golden
+    g = {int(v): int(w) for v, _n, w in golden("sqrt_variants.txt")}
+    assert first.item() == g[variant]           # SURVEY.md:38-40
 
 
 def test_sqrt_variant_r_runs_and_dummy_variants():

@@ -408,7 +408,7 @@ def _np_variant_rows(w, variant):
         xh = (f32(0.5) * x).astype(np.float32)
         y = (np.int32(0x5f3759df) - (x.view(np.int32) >> 1)).astype(np.int32).view(np.float32)
         for _ in range(3):
-            y = (y * (f32(1.5) - xh * (y * y))).astype(np.float32)
+            y = (y * (f32(1.5) - (xh * y) * y)).astype(np.float32)   # Quake's x2*y*y
         s = (x * y + f32(1e-4)).astype(np.float32)
     return np.maximum(np.floor((s - f32(0.5)).astype(np.float32)), 0).astype(np.int64)
 
@@ -479,3 +479,73 @@ def test_lambda_nodiag_reading_q2(orc):
         i = math.floor(math.sqrt(0.25 + 2 * w) + 0.5)             # Eq. 5's i-term (exact here)
         assert (i, w - i * (i - 1) // 2) == (int(I[w]), int(J[w]))
     assert (int(I[0]), int(J[0])) == (1, 0) and (int(I[2]), int(J[2])) == (2, 1)
+
+
+# ------------------------------------------------ sqrt variants: golden first failures
+def _golden_sqrt_variants():
+    return {int(vid): int(w) for vid, _name, w in golden("sqrt_variants.txt")}
+
+
+def _rn32(v):
+    """Round a non-negative rational to the nearest fp32 (ties to even), exactly."""
+    from fractions import Fraction
+    v = Fraction(v)
+    if v == 0:
+        return v
+    e = v.numerator.bit_length() - v.denominator.bit_length()
+    if Fraction(2) ** e > v:
+        e -= 1
+    ulp = Fraction(2) ** (e - 23)
+    q, r = divmod(v, ulp)
+    if r * 2 > ulp or (r * 2 == ulp and q % 2 == 1):
+        q += 1
+    return q * ulp
+
+
+def _sqrt32(x):
+    """Correctly rounded fp32 sqrt of an fp32 value x > 0 (integer square roots only)."""
+    from fractions import Fraction
+    from math import isqrt
+    E = 0                                      # 4^E <= x < 4^(E+1), so 2^E <= sqrt(x) < 2^(E+1)
+    while Fraction(4) ** (E + 1) <= x:
+        E += 1
+    while Fraction(4) ** E > x:
+        E -= 1
+    sc = Fraction(2) ** (23 - E)               # sqrt(x) * sc in [2^23, 2^24): one unit = one ulp
+    X = x * sc * sc
+    q = isqrt(X.numerator // X.denominator)    # floor(sqrt(X))
+    h = (Fraction(2 * q + 1, 2)) ** 2          # sqrt(X) vs q + 1/2  <=>  X vs (q + 1/2)^2
+    if X > h or (X == h and q % 2 == 1):
+        q += 1
+    return Fraction(q) / sc
+
+
+def _exact_row_x(w):
+    """lambda_X evaluated with exact rational arithmetic and explicit fp32 roundings."""
+    from fractions import Fraction
+    from math import floor
+    x = _rn32(Fraction(1, 4) + _rn32(2 * _rn32(w)))
+    s = _rn32(_sqrt32(x) - Fraction(1, 2))
+    return max(floor(s), 0)
+
+
+def test_sqrt_variant_golden_first_failures(orc):
+    """The oracle's scans hit the golden first failing omegas (SURVEY.md:38-40): 10,619,135
+    for lambda_X, 1,316,253 for lambda_N in the cited (x2*y)*y Newton order."""
+    g = _golden_sqrt_variants()
+    for vid, w_first in g.items():
+        nf, fw = orc.variant_scan(vid, 0, w_first + 1)
+        assert fw == w_first and nf == 1, (vid, nf, fw)
+    assert g[1] == T(4608) - 1 and g[2] == T(1622)
+
+
+def test_sqrt_variant_x_exact_rational_boundaries():
+    """Independent of numpy and of the oracle: lambda_X in exact rational arithmetic with
+    explicit round-to-nearest-even after each fp32 operation.  Eq. 3 holds at every row
+    boundary omega in {T(i) - 1, T(i)} below the golden omega, and fails there."""
+    g = _golden_sqrt_variants()[1]
+    for i in list(range(1, 64)) + list(range(4000, 4609)):
+        for w in (T(i) - 1, T(i)):
+            if w <= g:
+                r = _exact_row_x(w)
+                assert (T(r) <= w < T(r + 1)) == (w < g), (i, w, r)
