@@ -14,8 +14,11 @@
  *  - Argument validation is synchronous and returns a tri_status before any
  *    launch; a launch failure is reported as TRI_ECUDA (cudaGetLastError);
  *    kernel faults surface at the caller's next synchronization.
- *  - Every output buffer comes with its capacity in bytes; a capacity smaller
- *    than what the call writes returns TRI_EINVAL before any launch.
+ *  - Every buffer a kernel reads or writes comes with its capacity in bytes
+ *    (argument `<name>_bytes`); a capacity smaller than what the call reads or
+ *    writes returns TRI_EINVAL before any launch.  The only exceptions are the
+ *    peer-memory destinations of tri_ca_steps_p2p (addresses in another
+ *    process's allocation, sized by the owner) and the map self-check hooks.
  *  - Indices: cells (i, j) of the lower triangle 0 <= j <= i < n (P:86-87,
  *    P:189-199).  The PACKED layout of Eq. 1 stores cell (i, j) at T(i) + j,
  *    T(i) = i(i+1)/2; a rank's slice stores it at T(i) + j - out_offset.
@@ -51,11 +54,12 @@ typedef enum {
 } tri_status;
 
 enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2, TRI_LAMBDA_CLC = 7 };
-/* tri_collide only, rho = 256, 384 or 512 (384: this strategy only): the TRI_LAMBDA grid with
- * the filter gap evaluated on the
- * 5th-generation tensor cores (3xTF32 tcgen05.mma into TMEM, csrc/collide_tc.cu); the
- * count is the same exact fixed-order predicate (reading Q9). */
-enum { TRI_LAMBDA_TC = 8 };
+/* tri_collide only, rho = 256, 384 or 512 (384: these strategies only): the filter gap
+ * evaluated on the 5th-generation tensor cores (tcgen05.mma into TMEM,
+ * csrc/collide_tc.cu); the count is the same exact fixed-order predicate (reading Q9).
+ * TRI_LAMBDA_TC runs the TRI_LAMBDA grid (one CTA per tile omega), TRI_BB_TC the same
+ * tile body on the m x m BB grid -- the like-for-like comparator. */
+enum { TRI_LAMBDA_TC = 8, TRI_BB_TC = 9 };
 /* The paper's square-root variants of Eq. 4 (section 4.1), used WITHOUT
  * the integer correction: lambda_X = IEEE sqrtf, lambda_N = 0x5f3759df seed + 3
  * Newton steps + eps, lambda_R = x * rsqrtf(x) + eps, eps = 1e-4.  Exact only
@@ -151,55 +155,87 @@ tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode,
 
 /* Euclidean distance matrix: for this rank's packed slice,
  * d_out[T(i)+j - out_offset] = || p_i - p_j ||_2 in fp32 for j <= i (diag = 1).
- * d_pts: n points, point t at d_pts[t*ld .. t*ld+dim), dim in 1..4, ld >= dim.
- * Requires out_bytes >= 4 * out_cells, d_out 16-byte aligned; rho in {32,64,128,256}.
- * Stores are aligned 16-byte streaming stores; each 16-byte chunk of the slice
- * is written by exactly one thread. */
+ * d_pts: n points, point t at d_pts[t*ld .. t*ld+dim), dim in 1..4, ld >= dim;
+ * pts_bytes >= 4 * ((n-1)*ld + dim).  Requires out_bytes >= 4 * out_cells, d_out
+ * 16-byte aligned (32 at rho = 256); rho in {32,64,128,256}; strategy TRI_LAMBDA,
+ * TRI_BB, TRI_LAMBDA_PERSIST, TRI_LAMBDA_CLC or TRI_RB (world = 1); world > 1
+ * needs a snapped map (the rank's slice is contiguous).  Stores are aligned
+ * 16-byte streaming stores; each 16-byte chunk of the slice is written by exactly
+ * one thread. */
 tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts,
-                   int32_t dim, int64_t ld, float *d_out, size_t out_bytes, void *stream);
+                   int32_t dim, int64_t ld, size_t pts_bytes, float *d_out, size_t out_bytes,
+                   void *stream);
 
-/* Host-buffer EDM (end-to-end through the ABI): h_pts/h_out are HOST buffers
- * (pinned for overlap).  The packed output is produced in row bands of
- * ~band_cells cells into the caller's device workspace d_ws (ws_bytes >=
- * 2 * 4 * (band_cells + 4 * n)), and each band is copied to h_out while the
+/* Host-buffer EDM (end-to-end through the ABI): the same result as tri_edm with
+ * h_pts / h_out HOST buffers (pinned for overlap).  The points are uploaded to
+ * the caller's device buffer d_pts_ws (pts_ws_bytes >= 4 * n * ld); the packed
+ * output is produced in row bands (whole tile rows) of at most band_cells cells
+ * (0: as large as the workspace allows) into two halves of the caller's device
+ * workspace d_ws (32-byte aligned), and each band is copied to h_out while the
  * next one is computed (two CUDA streams created and destroyed by the call).
- * Synchronous: returns when h_out is complete.  d_pts_ws: device buffer of
- * n*ld floats for the uploaded points. */
+ * Synchronous: returns when h_out is complete.  Validation is tri_edm's
+ * (map, strategy -- TRI_RB excepted --, rho, dim, ld, pts_bytes = the host
+ * buffer's capacity, out_bytes = h_out's), plus: EINVAL when one tile row of
+ * the slice (rho rows, <= rho * row_end cells) does not fit one half of d_ws or
+ * in band_cells. */
 tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_pts,
-                        int32_t dim, int64_t ld, float *d_pts_ws, float *h_out,
-                        size_t out_bytes, void *d_ws, size_t ws_bytes, uint64_t band_cells);
+                        int32_t dim, int64_t ld, size_t pts_bytes, float *d_pts_ws,
+                        size_t pts_ws_bytes, float *h_out, size_t out_bytes, void *d_ws,
+                        size_t ws_bytes, uint64_t band_cells);
 
 /* Sphere collision count: *d_count (u64, zeroed by call) =
  * number of pairs j < i in this rank's omega tiles with
  *   d2 = fma(dz,dz, fma(dy,dy, dx*dx)) < (ri + rj)^2
  * evaluated in IEEE fp32 round-to-nearest with exactly that operation order.
- * d_spheres: n x 4 floats (x, y, z, r), 16-byte aligned.  rho in {128,256,512}.
- * The map must be built with diag = 1 (tiles) -- the strict filter is per pair. */
+ * d_spheres: n x 4 floats (x, y, z, r), 16-byte aligned, spheres_bytes >= 16 n.
+ * count_bytes >= 8.  rho in {128,256,512} (and 384 for TRI_LAMBDA_TC).
+ * The map must be built with diag = 1 (tiles) -- the strict filter is per pair.
+ * TRI_LAMBDA_TC / TRI_BB_TC need d_ws (tri_collide_workspace_size bytes, 16-byte
+ * aligned).  If a tensor-core or bulk-copy completion ever fails to arrive within ~2 s
+ * (it never should) the kernel sets bit 63 of *d_count and traps: the launch fails
+ * (TRI_ECUDA / a CUDA error at the next synchronization) and the count is marked
+ * invalid -- a real pair count is < 2^63. */
 tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
-                       unsigned long long *d_count, void *stream);
+                       size_t spheres_bytes, unsigned long long *d_count, size_t count_bytes,
+                       void *d_ws, size_t ws_bytes, void *stream);
+
+/* Device workspace tri_collide needs for `strategy` (bytes, 16-byte aligned; 0 for the
+ * SIMT strategies, which accept d_ws = NULL).  TRI_LAMBDA_TC / TRI_BB_TC: m * rho * 64
+ * bytes -- the TF32 row and column operands of every sphere (plus pad rows), written
+ * by the call's first kernel and read by the tiles with bulk (TMA) copies. */
+size_t tri_collide_workspace_size(const tri_map_t *map, int32_t strategy);
+
+/* Test hook: D = X Y^T (128 x 128, fp32, row-major) from ONE tcgen05.mma.kind::tf32
+ * 128 x 128 x 8 with the caller's operands (row-major 128 x 8 fp32, used as TF32: the
+ * low 13 mantissa bits are ignored).  It exposes the tensor core's fp32 accumulation
+ * error, which the TRI_LAMBDA_TC filter's margin assumes bounded by 2^-20 sum |x y|. */
+tri_status tri_tc_tf32_probe(const float *d_x, const float *d_y, float *d_d, void *stream);
 
 /* 1-D collision count (reading Q10): *d_count (u64, zeroed by
  * the call) = number of pairs j < i with |c_i - c_j| < r_i + r_j, evaluated in IEEE
  * fp32 as d = ci - cj, s = ri + rj, |d| < s.  d_intervals: n x 2 floats (c, r),
- * 8-byte aligned.  rho = 256.  TRI_LAMBDA launches the T(m-1) strictly-lower tiles
- * through Eq. 5 (tri_lambda_nodiag) then the m diagonal tiles; TRI_BB the m x m
- * grid.  Ranks split the T(m) tiles by the plain omega range (lambda) or by the
- * map's snapped tile rows (BB). */
+ * 8-byte aligned, intervals_bytes >= 8 n; count_bytes >= 8.  rho = 256.  TRI_LAMBDA
+ * launches the T(m-1) strictly-lower tiles through Eq. 5 (tri_lambda_nodiag) then
+ * the m diagonal tiles; TRI_BB the m x m grid.  Ranks split the T(m) tiles by the
+ * plain omega range (lambda) or by the map's snapped tile rows (BB). */
 tri_status tri_collide1d(const tri_map_t *map, int32_t strategy, const float *d_intervals,
-                         unsigned long long *d_count, void *stream);
+                         size_t intervals_bytes, unsigned long long *d_count, size_t count_bytes,
+                         void *stream);
 
 /* Device workspace tri_ca_step needs (bytes; may be 0). */
 size_t tri_ca_workspace_size(const tri_map_t *map);
 
 /* One synchronous generation of Life B3/S23 on the triangle (the
  * rule is Conway's, cells outside the triangle dead).  d_in/d_out: this rank's
- * packed slice (out_cells bytes, u8 {0,1}, 16-byte aligned, must not alias).
- * d_halo_above = row row_begin-1 (row_begin bytes) or NULL (dead); d_halo_below
- * = row row_end (row_end+1 bytes) or NULL (dead; ignored when row_end == n).
- * rho (tile edge) in {128, 224, 256, 512}.  d_ws: tri_ca_workspace_size bytes (NULL if 0). */
+ * packed slice (in_bytes, out_bytes >= out_cells; u8 {0,1}, 16-byte aligned,
+ * must not alias).  d_halo_above = row row_begin-1 (above_bytes >= row_begin)
+ * or NULL (dead); d_halo_below = row row_end (below_bytes >= row_end + 1) or
+ * NULL (dead; ignored when row_end == n).  rho (tile edge) in {128, 224, 256,
+ * 512}.  d_ws: tri_ca_workspace_size bytes (NULL if 0). */
 tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_in,
-                       uint8_t *d_out, const uint8_t *d_halo_above,
-                       const uint8_t *d_halo_below, void *d_ws, void *stream);
+                       size_t in_bytes, uint8_t *d_out, size_t out_bytes,
+                       const uint8_t *d_halo_above, size_t above_bytes,
+                       const uint8_t *d_halo_below, size_t below_bytes, void *d_ws, void *stream);
 
 /* k generations of the same rule in one call (temporal blocking, deep halos;
  * k in 1..16 at rho = 128, 1..8 at rho = 224): d_out = the state after k generations of the whole
@@ -207,12 +243,16 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
  * rank's rows (d_in) and of the k rows on either side.  d_halo_above = the
  * packed rows [max(row_begin - k, 0), row_begin) (contiguous in the owner's
  * slice) or NULL when row_begin == 0; d_halo_below = the packed rows
- * [row_end, min(row_end + k, n)) or NULL when row_end == n.  Each tile writes
- * only its own cells (partial 16-byte chunks byte-wise).  k = 1 computes the
- * same result as tri_ca_step.  HBM traffic per cell-generation ~2.2/k bytes. */
+ * [row_end, min(row_end + k, n)) or NULL when row_end == n.  Capacities:
+ * in_bytes, out_bytes >= out_cells; above_bytes >= T(row_begin) -
+ * T(max(row_begin - k, 0)); below_bytes >= T(min(row_end + k, n)) - T(row_end)
+ * (unchecked for a NULL halo).  Each tile writes only its own cells (partial
+ * 16-byte chunks byte-wise).  k = 1 computes the same result as tri_ca_step.
+ * HBM traffic per cell-generation ~2.2/k bytes. */
 tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in,
-                        uint8_t *d_out, const uint8_t *d_halo_above, const uint8_t *d_halo_below,
-                        void *d_ws, void *stream);
+                        size_t in_bytes, uint8_t *d_out, size_t out_bytes,
+                        const uint8_t *d_halo_above, size_t above_bytes,
+                        const uint8_t *d_halo_below, size_t below_bytes, void *d_ws, void *stream);
 
 /* tri_ca_steps with the halo exchange fused into the kernel's store phase
  * (peer-memory halo stores over NVLink instead of a
@@ -233,7 +273,9 @@ tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const
  * stream-ordered 4-byte all-reduce per epoch) and double-buffers the halo
  * buffers by epoch parity so a launch never writes a buffer a peer still reads. */
 tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in,
-                            uint8_t *d_out, const uint8_t *d_halo_above, const uint8_t *d_halo_below,
+                            size_t in_bytes, uint8_t *d_out, size_t out_bytes,
+                            const uint8_t *d_halo_above, size_t above_bytes,
+                            const uint8_t *d_halo_below, size_t below_bytes,
                             uint8_t *d_peer_above, uint8_t *d_peer_below, void *d_ws, void *stream);
 
 /* CUDA IPC for the peer buffers of tri_ca_steps_p2p (one process per GPU).
@@ -295,9 +337,11 @@ tri_status tet_map_eval_lut(uint64_t omega0, uint64_t count, uint32_t kmax, int3
  * with a = |x_p-x_q|^2, b = |x_q-x_s|^2, c = |x_s-x_p|^2,
  * P = (a+c-b)(a+b-c)(b+c-a); d_energy[t] (n doubles, zeroed by the call) +=
  * E/3 for t in {p, q, s}.  Terms in fp32, accumulation in fp64.
- * d_pts4: n x 4 floats (x, y, z, unused), 16-byte aligned. */
+ * d_pts4: n x 4 floats (x, y, z, unused), 16-byte aligned, pts_bytes >= 16 n;
+ * energy_bytes >= 8 n. */
 tri_status tet_triplet(const tet_map_t *map, int32_t strategy, const float *d_pts4,
-                       double nu, double *d_energy, void *stream);
+                       size_t pts_bytes, double nu, double *d_energy, size_t energy_bytes,
+                       void *stream);
 
 /* Number of kernels the most recent successful call on this host thread
  * enqueued (for the bench's launch accounting). */

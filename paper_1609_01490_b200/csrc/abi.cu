@@ -129,11 +129,14 @@ tri_status tri_lambda_nodiag(uint64_t omega, uint32_t *i, uint32_t *j) {
 }
 
 tri_status tri_collide1d(const tri_map_t *map, int32_t strategy, const float *d_intervals,
-                         unsigned long long *d_count, void *stream) {
+                         size_t intervals_bytes, unsigned long long *d_count, size_t count_bytes,
+                         void *stream) {
     g_launches = 0;
     if (bad_map(map) || (strategy != TRI_LAMBDA && strategy != TRI_BB) || !d_intervals || !d_count)
         return TRI_EINVAL;
     if (map->rho != 256 || (((uintptr_t)d_intervals) & 7u)) return TRI_EINVAL;
+    if (intervals_bytes / 8u < (uint64_t)map->n || count_bytes < 8 || (((uintptr_t)d_count) & 7u))
+        return TRI_EINVAL;
     return launch_collide1d(*map, strategy, d_intervals, d_count, (cudaStream_t)stream);
 }
 
@@ -176,30 +179,61 @@ tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode, void 
     return launch_dummy(*map, strategy, mode, d_out, (cudaStream_t)stream);
 }
 
+extern "C++" {
+namespace tri {
+// Validation shared by tri_edm and tri_edm_host (include/tri.h): the map, the
+// strategy, the tile edge, the point layout and both capacities.
+bool edm_args_bad(const tri_map_t *map, int32_t strategy, int32_t dim, int64_t ld, size_t pts_bytes,
+                  size_t out_bytes) {
+    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_RB && strategy != TRI_LAMBDA_CLC)) return true;
+    if (!map->diag || (map->world > 1 && !map->snap)) return true;
+    if (strategy == TRI_RB && map->world != 1) return true;
+    if (map->rho != 32 && map->rho != 64 && map->rho != 128 && map->rho != 256) return true;
+    if (dim < 1 || dim > 4 || ld < dim || ld > (1ll << 20)) return true;
+    const uint64_t need_pts = 4ull * ((uint64_t)(map->n - 1) * (uint64_t)ld + (uint64_t)dim);
+    if (pts_bytes < need_pts) return true;
+    if (out_bytes / 4u < map->out_cells) return true;
+    return false;
+}
+}  // namespace tri
+}  // extern "C++"
+
 tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts, int32_t dim, int64_t ld,
-                   float *d_out, size_t out_bytes, void *stream) {
+                   size_t pts_bytes, float *d_out, size_t out_bytes, void *stream) {
     g_launches = 0;
-    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_RB && strategy != TRI_LAMBDA_CLC) || !d_pts ||
-        !d_out)
-        return TRI_EINVAL;
-    if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
-    if (map->rho != 32 && map->rho != 64 && map->rho != 128 && map->rho != 256) return TRI_EINVAL;
-    if (dim < 1 || dim > 4 || ld < dim) return TRI_EINVAL;
+    if (!d_pts || !d_out || edm_args_bad(map, strategy, dim, ld, pts_bytes, out_bytes)) return TRI_EINVAL;
     if (((uintptr_t)d_out & (map->rho == 256 ? 31u : 15u)) != 0) return TRI_EINVAL;   // 32-B chunks at rho 256
-    if (out_bytes < map->out_cells * 4u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
     if (strategy == TRI_RB) return launch_edm_rb(*map, d_pts, dim, ld, d_out, (cudaStream_t)stream);
     return launch_edm(*map, strategy, d_pts, dim, ld, d_out, (cudaStream_t)stream);
 }
 
-tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres,
-                       unsigned long long *d_count, void *stream) {
+size_t tri_collide_workspace_size(const tri_map_t *map, int32_t strategy) {
+    if (bad_map(map)) return 0;
+    return (strategy == TRI_LAMBDA_TC || strategy == TRI_BB_TC) ? collide_tc_ws_bytes(*map) : 0;
+}
+
+tri_status tri_tc_tf32_probe(const float *d_x, const float *d_y, float *d_d, void *stream) {
     g_launches = 0;
-    if (bad_map(map) || (bad_strategy(strategy) && strategy != TRI_LAMBDA_TC) || !d_spheres || !d_count)
-        return TRI_EINVAL;
+    if (!d_x || !d_y || !d_d) return TRI_EINVAL;
+    return launch_tc_tf32_probe(d_x, d_y, d_d, (cudaStream_t)stream);
+}
+
+tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres, size_t spheres_bytes,
+                       unsigned long long *d_count, size_t count_bytes, void *d_ws, size_t ws_bytes,
+                       void *stream) {
+    g_launches = 0;
+    const bool tc = strategy == TRI_LAMBDA_TC || strategy == TRI_BB_TC;
+    if (bad_map(map) || (bad_strategy(strategy) && !tc) || !d_spheres || !d_count) return TRI_EINVAL;
     if (map->rho != 128 && map->rho != 256 && map->rho != 384 && map->rho != 512) return TRI_EINVAL;
-    if (map->rho == 384 && strategy != TRI_LAMBDA_TC) return TRI_EINVAL;      // tcgen05 tile edge only
-    if (((uintptr_t)d_spheres & 15u) != 0) return TRI_EINVAL;
+    if (map->rho == 384 && !tc) return TRI_EINVAL;                            // tcgen05 tile edge only
+    if (((uintptr_t)d_spheres & 15u) != 0 || (((uintptr_t)d_count) & 7u)) return TRI_EINVAL;
+    if (spheres_bytes / 16u < (uint64_t)map->n || count_bytes < 8) return TRI_EINVAL;
+    if (tc) {
+        if (!d_ws || ws_bytes < collide_tc_ws_bytes(*map) || (((uintptr_t)d_ws) & 15u)) return TRI_EINVAL;
+        if (map->rho == 128) return TRI_EINVAL;
+        return launch_collide_tc(*map, strategy, d_spheres, d_count, d_ws, (cudaStream_t)stream);
+    }
     return launch_collide(*map, strategy, d_spheres, d_count, (cudaStream_t)stream);
 }
 
@@ -208,12 +242,25 @@ size_t tri_ca_workspace_size(const tri_map_t *map) {
     return 0;
 }
 
-tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_in, uint8_t *d_out,
-                       const uint8_t *d_halo_above, const uint8_t *d_halo_below, void *d_ws,
-                       void *stream) {
+// Capacities of a CA call: state slices and the k-row halos (include/tri.h).
+static bool ca_bytes_bad(const tri_map_t *m, int32_t k, size_t in_bytes, size_t out_bytes, const void *above,
+                         size_t above_bytes, const void *below, size_t below_bytes) {
+    if (in_bytes < m->out_cells || out_bytes < m->out_cells) return true;
+    const uint64_t rb = (uint64_t)m->row_begin, re = (uint64_t)m->row_end, n = (uint64_t)m->n;
+    const uint64_t lo = rb > (uint64_t)k ? rb - (uint64_t)k : 0, hi = re + (uint64_t)k < n ? re + (uint64_t)k : n;
+    if (above && rb > 0 && above_bytes < T2(rb) - T2(lo)) return true;
+    if (below && re < n && below_bytes < T2(hi) - T2(re)) return true;
+    return false;
+}
+
+tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_in, size_t in_bytes,
+                       uint8_t *d_out, size_t out_bytes, const uint8_t *d_halo_above, size_t above_bytes,
+                       const uint8_t *d_halo_below, size_t below_bytes, void *d_ws, void *stream) {
     g_launches = 0;
     (void)d_ws;
     if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
+    if (ca_bytes_bad(map, 1, in_bytes, out_bytes, d_halo_above, above_bytes, d_halo_below, below_bytes))
+        return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
     if (map->rho != 128 && map->rho != 224 && map->rho != 256 && map->rho != 512) return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
@@ -221,27 +268,33 @@ tri_status tri_ca_step(const tri_map_t *map, int32_t strategy, const uint8_t *d_
     return launch_ca(*map, strategy, d_in, d_out, d_halo_above, d_halo_below, (cudaStream_t)stream);
 }
 
-tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in, uint8_t *d_out,
-                        const uint8_t *d_halo_above, const uint8_t *d_halo_below, void *d_ws, void *stream) {
+tri_status tri_ca_steps(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in, size_t in_bytes,
+                        uint8_t *d_out, size_t out_bytes, const uint8_t *d_halo_above, size_t above_bytes,
+                        const uint8_t *d_halo_below, size_t below_bytes, void *d_ws, void *stream) {
     g_launches = 0;
     (void)d_ws;
     if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
     if (k < 1 || !((map->rho == 128 && k <= 16) || (map->rho == 224 && k <= 8))) return TRI_EINVAL;
+    if (ca_bytes_bad(map, k, in_bytes, out_bytes, d_halo_above, above_bytes, d_halo_below, below_bytes))
+        return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out)) & 15u) return TRI_EINVAL;
     if (map->out_cells == 0) return TRI_OK;
     return launch_ca_steps(*map, strategy, k, d_in, d_out, d_halo_above, d_halo_below, nullptr, nullptr,
                            (cudaStream_t)stream);
 }
 
-tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in, uint8_t *d_out,
-                            const uint8_t *d_halo_above, const uint8_t *d_halo_below, uint8_t *d_peer_above,
-                            uint8_t *d_peer_below, void *d_ws, void *stream) {
+tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, const uint8_t *d_in,
+                            size_t in_bytes, uint8_t *d_out, size_t out_bytes, const uint8_t *d_halo_above,
+                            size_t above_bytes, const uint8_t *d_halo_below, size_t below_bytes,
+                            uint8_t *d_peer_above, uint8_t *d_peer_below, void *d_ws, void *stream) {
     g_launches = 0;
     (void)d_ws;
     if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || d_in == d_out) return TRI_EINVAL;
     if (!map->diag || (map->world > 1 && !map->snap)) return TRI_EINVAL;
     if (k < 1 || !((map->rho == 128 && k <= 16) || (map->rho == 224 && k <= 8))) return TRI_EINVAL;
+    if (ca_bytes_bad(map, k, in_bytes, out_bytes, d_halo_above, above_bytes, d_halo_below, below_bytes))
+        return TRI_EINVAL;
     if ((((uintptr_t)d_in) | ((uintptr_t)d_out) | ((uintptr_t)d_peer_above) | ((uintptr_t)d_peer_below)) & 15u)
         return TRI_EINVAL;
     // every peer row this rank sends must be its own: it owns >= k rows (or none)
@@ -343,10 +396,13 @@ tri_status tet_map_eval_lut(uint64_t omega0, uint64_t count, uint32_t kmax, int3
     return launch_tet_map_eval_lut(omega0, count, kmax, shift, d_lut, d_ijk, d_fail, (cudaStream_t)stream);
 }
 
-tri_status tet_triplet(const tet_map_t *map, int32_t strategy, const float *d_pts4, double nu,
-                       double *d_energy, void *stream) {
+tri_status tet_triplet(const tet_map_t *map, int32_t strategy, const float *d_pts4, size_t pts_bytes, double nu,
+                       double *d_energy, size_t energy_bytes, void *stream) {
     g_launches = 0;
     if (!map || bad_strategy(strategy) || !d_pts4 || !d_energy) return TRI_EINVAL;
+    if (map->n < 3 || pts_bytes / 16u < (uint64_t)map->n || energy_bytes / 8u < (uint64_t)map->n ||
+        (((uintptr_t)d_energy) & 7u))
+        return TRI_EINVAL;
     if (map->n < 3 || map->m != (map->n + map->rho - 1) / map->rho || map->blocks != T3((uint64_t)map->m) ||
         map->omega_end > map->blocks || map->omega_begin > map->omega_end)
         return TRI_EINVAL;

@@ -267,7 +267,6 @@ tri_status launch_collide(const tri_map_t &m, int strategy, const float *sph, un
     a.omega_end = m.omega_end;
     a.tile_row_begin = 0;
     a.count = count;
-    if (strategy == TRI_LAMBDA_TC) return launch_collide_tc(m, sph, count, st);     // collide_tc.cu
     switch (m.rho) {
         case 128: return launch_r<128>(m, strategy, a, st);
         case 256: return launch_r<256>(m, strategy, a, st);

@@ -1,46 +1,58 @@
-// collide_tc.cu -- TRI_LAMBDA_TC for tri_collide (rho = 256, 384 or 512): the collision
-// filter gap of collide.cu evaluated on the 5th-generation tensor cores.
+// collide_tc.cu -- TRI_LAMBDA_TC / TRI_BB_TC for tri_collide (rho = 256, 384 or 512): the
+// collision filter of reading Q9 evaluated on the 5th-generation tensor cores.
 //
-//   g_ij = A'_i + A'_j - 2 (x_i x_j + y_i y_j + z_i z_j + r_i r_j) = X_i . Y_j,
-//   X_i = (x, y, z, r, A'_i, 1, 0, 0),  Y_j = (-2x, -2y, -2z, -2r, 1, A'_j, 0, 0)
+// The count is the fixed-order fp32 predicate d2 < s*s over j < i (reading
+// Q9).  The tensor cores only FILTER: a pair the predicate counts always gets a negative
+// filter value, and every (row, 32-column group) with a negative value is re-examined
+// with the exact predicate, so the count is exact.
 //
-// is a K = 8 contraction over the tile.  TF32 keeps 11 significant bits, so each
-// operand is split into big + small TF32 parts and the tile is accumulated in
-// TMEM from three kind::tf32 MMAs (X_big Y_big + X_big Y_small + X_small Y_big,
-// 128 x 256 x 8 each): products of TF32 values are exact in fp32, the dropped
-// small.small term is <= 2^-21 (M_i + M_j) and the fp32 accumulation adds a few
-// ulps of sum |terms| <= 2 (M_i + M_j).  A' carries kappa u M with kappa u = 2^-15,
-// so every pair the fixed-order predicate (reading Q9) counts still has g < 0;
-// the epilogue ORs the sign bits of each row's 32-column groups and recounts a
-// flagged group with the exact scalar predicate, so the count is exact.
+// Filter (one kind::tf32 MMA per 128 x 128 block, K = 8, every operand exact in TF32):
+//   q_i  = tf32(p_i - c), c = (1/2, 1/2, 1/2)           quantised, centred position
+//   e_i  = |p_i - (q_i + c)|                            its exact Euclidean error (fp64)
+//   R_i  = tf32_up(r_i (1 + 8u) + e_i)                  inflated radius, u = 2^-24
+//   A_i  = |q_i|^2 - R_i^2 - kappa u M_i,  M_i = |q_i|^2 + R_i^2   (fp64), split into
+//          A_i = Ab_i + As_i + res_i with Ab, As TF32 and |res_i| <= 2^-21 M_i
+//   X_i  = ( qx,  qy,  qz,  R, Ab, As, 1, 1)            row operand (A, K-major)
+//   Y_j  = (-2qx,-2qy,-2qz,-2R, 1,  1, Ab, As)          column operand (B, K-major)
+//   g_ij = X_i . Y_j = |q_i - q_j|^2 - (R_i + R_j)^2 - kappa u (M_i + M_j) - res_i - res_j
+// Why it is conservative: the fp32 predicate counts only if the real distance satisfies
+// d < (1 + 4.1u)(r_i + r_j) (three roundings in d2, two in s*s); then |q_i - q_j| <=
+// d + e_i + e_j < R_i + R_j, so the exact value of X_i . Y_j is < -kappa u (M_i + M_j) +
+// 2^-21 (M_i + M_j).  Products of TF32 values are exact in fp32; the tensor core's fp32
+// sum of the 8 products is within 2^-20 sum_k |X_ik Y_jk| <= 2^-20 * 2.01 (M_i + M_j) of
+// the exact sum (the accumulation bound, measured on B200 by tri_tc_tf32_probe and
+// tests/test_gpu_parity.py::test_tc_tf32_accumulation_bound on adversarial cancelling
+// operands).  With kappa u = 2^-16 the computed g_ij is therefore < 0.
 //
-// CTA = 128 threads (4 warps) per lambda tile; the tile is (rho/128)^2 blocks of
-// 128 x 128, each one M = 128, N = 128 accumulator pass over 128 TMEM columns
-// (larger tiles amortise the TMEM allocation and barrier set-up: rho = 256 2.83 ms,
-// 512 2.41 ms (74 KB smem: 3 CTAs per SM), 384 2.24 ms (55 KB: 4 CTAs, as many as
-// can hold their 128 TMEM columns at once)).
-// Operands: K-major, no swizzle, canonical 8-row x 16-byte core matrices
-// (LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups).
-// Diagonal tiles (strict j < i) are counted with the scalar predicate.
+// Layout: tri_collide's caller-owned workspace holds X and Y for m * rho rows (pad rows
+// past n make every g positive) as canonical K-major no-swizzle core matrices: 8-row
+// group g at byte 256 g, K half h at +128 h, row r at +16 r -- so a tile's operands are
+// ONE contiguous rho x 32-byte run each, staged into shared memory by two 1-D bulk
+// copies (cp.async.bulk, the TMA engine) completing on an mbarrier.
+//
+// CTA = 128 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB
+// grid); 128 TMEM columns (4 CTAs per SM hold all 512); per 128 x 128 block
+// one tcgen05.mma (issued by one thread), commit -> mbarrier, then the epilogue:
+// thread t = accumulator lane t = row t of the block, tcgen05.ld 32 columns at a time,
+// sign bits OR-ed by LOP3 (ALU pipe) and counted by IMAD.HI (FMA pipe) so both pipes
+// share the work.  A flagged 32-column group recounts only its negative columns, from
+// registers.  Diagonal tiles skip the blocks above the diagonal and recount j < i only.
 #include "tri_common.cuh"
 
 namespace {
 
+constexpr int kThreads = 128, kCols = 128;
+constexpr double kKappaU = 1.0 / 65536.0;               // 2^-16
+constexpr float kPad = 1.0e30f;                         // pad-row operand: g = 1e30 > 0
+
 struct TcArgs {
     const float4 *sph;
-    int64_t n;
+    const uint32_t *ops;          // workspace: X rows [0, npad), then Y rows [0, npad)
+    int64_t n, npad;
     uint64_t omega_begin, omega_end;
     unsigned long long *count;
+    uint32_t two;                 // = 2, a runtime value so ptxas keeps IMAD.HI (FMA pipe)
 };
-
-constexpr int kThreads = 128, kCols = 128;   // accumulator: 128 lanes x 128 fp32 columns
-constexpr float kKappaU = 1.0f / 32768.0f;     // 2^-15
-
-__device__ __forceinline__ float4 load_sph(const TcArgs &a, int64_t idx) {
-    if (idx < a.n) return __ldg(a.sph + idx);
-    const float nan = __int_as_float(0x7fffffff);
-    return make_float4(nan, nan, nan, nan);
-}
 
 // The ABI's exact fixed-order predicate (reading Q9).
 __device__ __forceinline__ uint32_t hit(const float4 p, const float4 q) {
@@ -50,41 +62,79 @@ __device__ __forceinline__ uint32_t hit(const float4 p, const float4 q) {
     return d2 < __fmul_rn(s, s) ? 1u : 0u;
 }
 
-__device__ __forceinline__ float a_prime(const float4 c) {
-    const float q = fmaf(c.z, c.z, fmaf(c.y, c.y, c.x * c.x));
-    const float w = c.w * c.w;
-    return fmaf(-kKappaU, q + w, q - w);
-}
-
-__device__ __forceinline__ uint32_t tf32(float x) {
+__device__ __forceinline__ float tf32_rn(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
+    return __uint_as_float(r);
 }
 
-template <int kRho>
-struct __align__(128) Smem {
-    // operand rows: 32 B (K = 8 tf32) each, in the canonical core-matrix order
-    uint32_t xb[kRho / 8][2][8][4], xs[kRho / 8][2][8][4];     // rows (A): big / small
-    uint32_t yb[kRho / 8][2][8][4], ys[kRho / 8][2][8][4];     // cols (B): big / small
-    float4 col[kRho];                                           // column spheres (exact recount)
-    unsigned long long mbar;
-    uint32_t taddr;
-};
+// smallest TF32 value >= x (x >= 0, finite)
+__device__ __forceinline__ float tf32_up(float x) {
+    uint32_t b = __float_as_uint(x);
+    if (b & 0x1fffu) b = (b | 0x1fffu) + 1u;
+    return __uint_as_float(b);
+}
 
-// store one operand row (8 values) split into big / small at row r of a [group][khalf][8][4] array
-__device__ __forceinline__ void put_row(uint32_t (*big)[2][8][4], uint32_t (*sml)[2][8][4], int r,
-                                        const float (&v)[8]) {
+// canonical K-major core-matrix slot of element k of row r
+__device__ __forceinline__ int slot(int64_t r, int k) {
+    return (int)(((r >> 3) * 64) + ((k >> 2) * 32) + ((r & 7) * 4) + (k & 3));
+}
+
+// ---------------------------------------------------------------- operand preparation
+// One thread per row of [0, npad): the quantities of the header, in fp64 where an error
+// bound is computed, written as TF32 bit patterns.  Thread 0 also zeroes the count.
+__global__ void collide_tc_prep(const float4 *__restrict__ sph, int64_t n, int64_t npad, uint32_t *__restrict__ ops,
+                                unsigned long long *count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *count = 0ull;
+    if (i >= npad) return;
+    float x[8], y[8];
+    if (i < n) {
+        const float4 p = __ldg(sph + i);
+        const float qx = tf32_rn(__fsub_rn(p.x, 0.5f)), qy = tf32_rn(__fsub_rn(p.y, 0.5f)),
+                    qz = tf32_rn(__fsub_rn(p.z, 0.5f));
+        // exact error of the quantised position: p, q and 1/2 are fp32, so every
+        // difference and sum below is exact in fp64 (up to the final sqrt / square)
+        const double ex = (double)p.x - ((double)qx + 0.5), ey = (double)p.y - ((double)qy + 0.5),
+                     ez = (double)p.z - ((double)qz + 0.5);
+        const double e = sqrt(ex * ex + ey * ey + ez * ez) * (1.0 + 0x1p-40) + 0x1p-60;
+        const double r = fabs((double)p.w) * (1.0 + 0x1p-21) + e;     // (1 + 8u) r + e, rounded up below
+        const float R = tf32_up(__double2float_ru(r));
+        const double q2 = (double)qx * qx + (double)qy * qy + (double)qz * qz, R2 = (double)R * R;
+        const double A = q2 - R2 - kKappaU * (q2 + R2);
+        const float ab = tf32_rn((float)A);
+        const float as = tf32_rn((float)(A - (double)ab));
+        x[0] = qx; x[1] = qy; x[2] = qz; x[3] = R; x[4] = ab; x[5] = as; x[6] = 1.f; x[7] = 1.f;
+        y[0] = -2.f * qx; y[1] = -2.f * qy; y[2] = -2.f * qz; y[3] = -2.f * R; y[4] = 1.f; y[5] = 1.f;
+        y[6] = ab; y[7] = as;
+        if (A != A) {                                  // NaN: the predicate never counts it -> a pad row
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
+            x[4] = kPad;
+            y[6] = kPad;
+        } else if (!(fabs(A) < 1e30)) {                // huge: flagged against every real row / column
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
+            x[4] = -kPad;
+            y[4] = 1.f;
+            y[6] = -kPad;
+        }
+    } else {                                           // pad row / column: g = 1e30 against real ones
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
+        x[4] = kPad;
+        y[6] = kPad;
+    }
+    uint32_t *X = ops, *Y = ops + npad * 8;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const uint32_t b = tf32(v[k]);
-        big[r >> 3][k >> 2][r & 7][k & 3] = b;
-        sml[r >> 3][k >> 2][r & 7][k & 3] = tf32(v[k] - __uint_as_float(b));
+        X[slot(i, k)] = __float_as_uint(x[k]);
+        Y[slot(i, k)] = __float_as_uint(y[k]);
     }
 }
 
-__device__ __forceinline__ uint64_t smem_desc(const void *p) {
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(p);
+// ---------------------------------------------------------------- tcgen05 / TMA helpers
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3fff);            // start address
     d |= (uint64_t)(128 >> 4) << 16;                  // LBO: next K half
@@ -93,19 +143,23 @@ __device__ __forceinline__ uint64_t smem_desc(const void *p) {
     return d;                                         // base offset 0, lbo mode 0, SWIZZLE_NONE
 }
 
-// kind::tf32, fp32 accumulator, K-major A and B, M = 128, N = 256
+// kind::tf32, fp32 accumulator, K-major A and B, M = 128, N = kCols
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCols >> 3) << 17) |
                             ((uint32_t)(128 >> 4) << 24);
 
-__device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t accumulate) {
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-        "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(0), "r"(kIdesc));
 }
 
-__device__ __forceinline__ bool mbar_wait(uint32_t mb, uint32_t parity) {
-    for (int it = 0; it < (1 << 18); ++it) {
+// Wait for an mbarrier phase.  A completion that never arrives (a broken tensor-core or
+// copy path) must not hang the GPU or leave a plausible count: after ~2 s the count gets
+// its sticky invalid bit 63 (include/tri.h) and the kernel traps.
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity, unsigned long long *count) {
+    long long t0 = 0;
+    for (int it = 0;; ++it) {
         uint32_t done;
         asm volatile(
             "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -113,154 +167,259 @@ __device__ __forceinline__ bool mbar_wait(uint32_t mb, uint32_t parity) {
             : "=r"(done)
             : "r"(mb), "r"(parity)
             : "memory");
-        if (done) return true;
+        if (done) return;
+        if (it == 64) t0 = clock64();
+        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > 4000000000ll) {
+            if (count) atomicOr(count, 1ull << 63);
+            __trap();
+        }
     }
-    return false;
 }
 
-template <int kRho>
-__global__ void __launch_bounds__(kThreads) collide_tc_kernel(TcArgs a) {
-    extern __shared__ __align__(128) unsigned char dsm[];
-    Smem<kRho> &sm = *reinterpret_cast<Smem<kRho> *>(dsm);
-    const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
-    if (w >= a.omega_end) return;
-    uint32_t bi, bj;
-    tri::lambda_map(w, bi, bj);
-    const int t = threadIdx.x, warp = t >> 5;
-    const int64_t r0 = (int64_t)bi * kRho, c0 = (int64_t)bj * kRho;
-    uint32_t cnt = 0;
+__device__ __forceinline__ void ldtm32(uint32_t ta, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
+        : "r"(ta));
+}
 
-    // columns: spheres for the recount, Y big / small operand rows
+// Nonzero iff some value of the group has its sign bit set.  kFma of the 32 values are
+// tested on the FMA pipe (hi(2 v) = v >> 31 by IMAD.HI, summed), the rest by 3-input
+// LOP3 ORs on the ALU pipe.
+template <int kFma>
+__device__ __forceinline__ uint32_t any_negative(const uint32_t (&v)[32], uint32_t two) {
+    constexpr int kAlu = 32 - kFma;
+    static_assert(kAlu >= 3 && (kAlu - 3) % 2 == 0, "ALU share: 3 + 2k values");
+    uint32_t o;
+    asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(v[0]), "r"(v[1]), "r"(v[2]));
 #pragma unroll
-    for (int h = 0; h < kRho / kThreads; ++h) {
-        const int j = t + kThreads * h;
-        const float4 c = load_sph(a, c0 + j);
-        sm.col[j] = c;
-        const float v[8] = {-2.f * c.x, -2.f * c.y, -2.f * c.z, -2.f * c.w, 1.f, a_prime(c), 0.f, 0.f};
-        put_row(sm.yb, sm.ys, j, v);
+    for (int e = 3; e < kAlu; e += 2) asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(o), "r"(v[e]), "r"(v[e + 1]));
+    uint32_t c = o >> 31;
+#pragma unroll
+    for (int e = kAlu; e < 32; ++e) asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(c) : "r"(v[e]), "r"(two), "r"(c));
+    return c;
+}
+
+// bit e set iff value e of the group is negative (only for flagged groups: rare)
+__device__ __forceinline__ uint32_t neg_mask(const uint32_t (&v)[32]) {
+    uint32_t msk = 0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) msk |= (v[e] >> 31) << e;
+    return msk;
+}
+
+// the exact predicate on the negative columns of one flagged group, j0 + e for the set
+// bits e of msk below jlim (rare: not inlined, keeps the hot loop small)
+__device__ __noinline__ uint32_t recount(const float4 *sph, int64_t n, uint32_t msk, int64_t i, int64_t j0,
+                                         int jlim) {
+    if (jlim < 32) msk &= jlim <= 0 ? 0u : (1u << jlim) - 1u;
+    if (!msk || i >= n) return 0;
+    const float4 p = __ldg(sph + i);
+    uint32_t cnt = 0;
+    while (msk) {
+        const int e = __ffs(msk) - 1;
+        msk &= msk - 1;
+        if (j0 + e < n) cnt += hit(p, __ldg(sph + j0 + e));
     }
-    if (bi == bj) {                                      // diagonal tile: strict j < i, scalar exact
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < kRho / kThreads; ++h) {
-            const int i = t + kThreads * h;
-            const float4 p = load_sph(a, r0 + i);
-#pragma unroll 4
-            for (int j = 0; j < i; ++j) cnt += hit(p, sm.col[j]);
-        }
+    return cnt;
+}
+
+template <int kRho, bool kBB, int kFma>
+__global__ void __launch_bounds__(kThreads, 4) collide_tc_kernel(TcArgs a) {
+    constexpr int R = kRho / 128;
+    constexpr uint32_t kOpBytes = kRho * 32;
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    __shared__ __align__(8) unsigned long long mbar[2];     // [0] operands landed, [1] MMA done
+    __shared__ uint32_t taddr;
+    uint32_t bi, bj;
+    if (kBB) {                                         // m x m grid: blocks above the diagonal exit
+        bj = blockIdx.x;
+        bi = blockIdx.y;
+        if (bj > bi) return;
+        const uint64_t w = tri::T2(bi) + bj;
+        if (w < a.omega_begin || w >= a.omega_end) return;
     } else {
-        // rows: X big / small operand rows (all 256; pass p uses rows 128 p ..)
-        float4 prow[kRho / kThreads];
-#pragma unroll
-        for (int h = 0; h < kRho / kThreads; ++h) {
-            const int i = t + kThreads * h;
-            const float4 p = load_sph(a, r0 + i);
-            prow[h] = p;
-            const float v[8] = {p.x, p.y, p.z, p.w, a_prime(p), 1.f, 0.f, 0.f};
-            put_row(sm.xb, sm.xs, i, v);
-        }
-        const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
-        if (warp == 0) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(&sm.taddr)),
-                         "n"(kCols));
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        }
-        if (t == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        // generic-proxy smem writes -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t tmem = sm.taddr;
-        bool ok = true;
+        const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (w >= a.omega_end) return;
+        tri::lambda_map(w, bi, bj);
+    }
+    const int t = threadIdx.x, warp = t >> 5;
+    const uint32_t xs = (uint32_t)__cvta_generic_to_shared(dsm), ys = xs + kOpBytes;
+    const uint32_t mb_ld = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+    const uint32_t mb_mma = (uint32_t)__cvta_generic_to_shared(&mbar[1]);
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_ld));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_mma));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the tile's operand rows: two contiguous runs of the workspace -> shared memory
+        const uint32_t *gx = a.ops + (int64_t)bi * kRho * 8, *gy = a.ops + (a.npad + (int64_t)bj * kRho) * 8;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb_ld), "r"(2 * kOpBytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(xs),
+            "l"(gx), "r"(kOpBytes), "r"(mb_ld)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ys),
+            "l"(gy), "r"(kOpBytes), "r"(mb_ld)
+            : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&taddr)),
+                     "n"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = taddr;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    if (t == 0) mbar_wait(mb_ld, 0, a.count);
+    const bool diag = bi == bj;
+    uint32_t cnt = 0, phase = 0;
 #pragma unroll 1
-        for (int pass = 0; pass < (kRho / 128) * (kRho / 128); ++pass) {
-            const int rh = pass / (kRho / 128), ch = pass % (kRho / 128);   // 128-row, 128-column block
+    for (int rh = 0; rh < R; ++rh) {
+        const int64_t i = (int64_t)bi * kRho + rh * 128 + t;        // this thread's row
+#pragma unroll 1
+        for (int ch = 0; ch < (diag ? rh + 1 : R); ++ch) {
             if (t == 0) {
-                const int g0 = rh * 16, h0 = ch * 16;       // first 8-row groups of the A and B halves
-                mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.yb[h0]), 0u);
-                mma(tmem, smem_desc(&sm.xb[g0]), smem_desc(&sm.ys[h0]), 1u);
-                mma(tmem, smem_desc(&sm.xs[g0]), smem_desc(&sm.yb[h0]), 1u);
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    mb));
-            }
-            ok = mbar_wait(mb, (uint32_t)(pass & 1)) && ok;
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            // epilogue: thread t = accumulator lane t = row 128 pass + t; 8 groups of 32 columns
-            uint32_t flags = 0;
-#pragma unroll
-            for (int cg = 0; cg < kCols / 32; ++cg) {
-                uint32_t v[32];
-                const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cg * 32);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                mma(tmem, smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
                 asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-                    "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(ta));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                uint32_t o = 0;                             // OR of 32 sign bits, 3-input LOP3s
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_mma)
+                    : "memory");
+            }
+            mbar_wait(mb_mma, phase, a.count);
+            phase ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int64_t j0 = (int64_t)bj * kRho + ch * 128;
+            // strict j < i inside a diagonal block: columns [0, t) of the block's 128
+            const int jlim = (diag && ch == rh) ? t : 128;
 #pragma unroll
-                for (int e = 0; e < 32; e += 2)
-                    asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(o), "r"(v[e]), "r"(v[e + 1]));
-                flags |= (o >> 31) << cg;
+            for (int cg = 0; cg < kCols / 32; cg += 2) {
+                uint32_t v0[32], v1[32];
+                ldtm32(lane_base + (uint32_t)(cg * 32), v0);
+                ldtm32(lane_base + (uint32_t)(cg * 32 + 32), v1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const uint32_t f0 = any_negative<kFma>(v0, a.two), f1 = any_negative<kFma>(v1, a.two);
+                if (f0 | f1) {
+                    if (f0) cnt += recount(a.sph, a.n, neg_mask(v0), i, j0 + cg * 32, jlim - cg * 32);
+                    if (f1) cnt += recount(a.sph, a.n, neg_mask(v1), i, j0 + cg * 32 + 32, jlim - cg * 32 - 32);
+                }
             }
-            // rare: the exact predicate on this row's flagged 32-column groups
-            const float4 p = prow[rh];
-#pragma unroll 1
-            while (flags) {
-                const int cg = __ffs(flags) - 1;
-                flags &= flags - 1;
-#pragma unroll 4
-                for (int j = 128 * ch + 32 * cg; j < 128 * ch + 32 * cg + 32; ++j) cnt += hit(p, sm.col[j]);
-            }
-            // every lane's loads are done before pass 1 overwrites the accumulator
+            // every lane's loads are done before the next MMA overwrites the accumulator
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncthreads();
-            asm volatile("tcgen05.fence::after_thread_sync;");
         }
-        if (warp == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
-        // an MMA completion that never arrived (bounded wait): poison the count, never hang
-        if (!ok && t == 0) atomicAdd(a.count, 1ull << 62);
     }
-    // count: warp reduce, one atomic per warp (skipped if 0)
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((t & 31) == 0 && cnt) atomicAdd(a.count, (unsigned long long)cnt);
+}
+
+// ---------------------------------------------------------------- accumulation probe
+// D = X Y^T for one 128 x 128 x 8 block with caller-given TF32 operands (row-major
+// 128 x 8 each): the raw tensor-core fp32 result, for the accumulation-bound test.
+__global__ void __launch_bounds__(kThreads) tc_tf32_probe_kernel(const float *x, const float *y, float *d) {
+    __shared__ __align__(1024) uint32_t sx[128 * 8], sy[128 * 8];
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ uint32_t taddr;
+    const int t = threadIdx.x, warp = t >> 5;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        sx[slot(t, k)] = __float_as_uint(x[t * 8 + k]);
+        sy[slot(t, k)] = __float_as_uint(y[t * 8 + k]);
+    }
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&taddr)),
+                     "n"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = taddr;
+    if (t == 0) {
+        mma(tmem, smem_desc((uint32_t)__cvta_generic_to_shared(sx)), smem_desc((uint32_t)__cvta_generic_to_shared(sy)));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb)
+                     : "memory");
+    }
+    mbar_wait(mb, 0, nullptr);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+    for (int cg = 0; cg < kCols / 32; ++cg) {
+        uint32_t v[32];
+        ldtm32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cg * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < 32; ++e) d[t * 128 + cg * 32 + e] = __uint_as_float(v[e]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
 }
 
 }  // namespace
 
 namespace tri {
 
-template <int kRho>
-static void launch_rho(TcArgs a, uint64_t nb, cudaStream_t st) {
-    const int smem = (int)sizeof(Smem<kRho>);
-    cudaFuncSetAttribute(collide_tc_kernel<kRho>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    collide_tc_kernel<kRho><<<tile_grid(nb), kThreads, smem, st>>>(a);
+constexpr int kFmaShare = 9;          // values per 32 tested on the FMA pipe (A/B'd on B200)
+
+size_t collide_tc_ws_bytes(const tri_map_t &m) { return (size_t)m.m * (size_t)m.rho * 64u; }
+
+template <int kRho, bool kBB>
+static void launch_rho(const tri_map_t &m, TcArgs a, cudaStream_t st) {
+    // pad the dynamic smem so at most 4 CTAs share an SM: they hold all 512 TMEM columns
+    const int smem = 2 * kRho * 32 > 48 * 1024 ? 2 * kRho * 32 : 48 * 1024;
+    auto k = collide_tc_kernel<kRho, kBB, kFmaShare>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), kThreads, smem, st>>>(a);
+    else k<<<tile_grid(a.omega_end - a.omega_begin), kThreads, smem, st>>>(a);
 }
 
-tri_status launch_collide_tc(const tri_map_t &m, const float *sph, unsigned long long *count, cudaStream_t st) {
+tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph, unsigned long long *count,
+                             void *ws, cudaStream_t st) {
     if (m.rho != 256 && m.rho != 384 && m.rho != 512) return TRI_EINVAL;
+    if (strategy == TRI_BB_TC && m.m > 65535) return TRI_EINVAL;
     TcArgs a;
     a.sph = (const float4 *)sph;
+    a.ops = (const uint32_t *)ws;
     a.n = m.n;
+    a.npad = m.m * (int64_t)m.rho;
     a.omega_begin = m.omega_begin;
     a.omega_end = m.omega_end;
     a.count = count;
-    if (cudaMemsetAsync(count, 0, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
-    const uint64_t nb = a.omega_end - a.omega_begin;
-    if (!nb) return TRI_OK;
-    if (m.rho == 512) launch_rho<512>(a, nb, st);
-    else if (m.rho == 384) launch_rho<384>(a, nb, st);
-    else launch_rho<256>(a, nb, st);
+    a.two = 2u;
+    collide_tc_prep<<<(unsigned)((a.npad + 255) / 256), 256, 0, st>>>(a.sph, a.n, a.npad, (uint32_t *)ws, count);
+    note_launches(1);
+    if (a.omega_end > a.omega_begin) {
+        const bool bb = strategy == TRI_BB_TC;
+        if (m.rho == 512) bb ? launch_rho<512, true>(m, a, st) : launch_rho<512, false>(m, a, st);
+        else if (m.rho == 384) bb ? launch_rho<384, true>(m, a, st) : launch_rho<384, false>(m, a, st);
+        else bb ? launch_rho<256, true>(m, a, st) : launch_rho<256, false>(m, a, st);
+        note_launches(1);
+    }
+    return cuda_status();
+}
+
+tri_status launch_tc_tf32_probe(const float *x, const float *y, float *d, cudaStream_t st) {
+    tc_tf32_probe_kernel<<<1, kThreads, 0, st>>>(x, y, d);
     note_launches(1);
     return cuda_status();
 }

@@ -289,13 +289,23 @@ tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int di
 // Row bands (multiples of rho rows) are computed into a ping-pong device
 // workspace and copied to the host buffer while the next band computes.
 extern "C" tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_pts, int32_t dim,
-                                   int64_t ld, float *d_pts_ws, float *h_out, size_t out_bytes, void *d_ws,
-                                   size_t ws_bytes, uint64_t band_cells) {
+                                   int64_t ld, size_t pts_bytes, float *d_pts_ws, size_t pts_ws_bytes,
+                                   float *h_out, size_t out_bytes, void *d_ws, size_t ws_bytes,
+                                   uint64_t band_cells) {
     using namespace tri;
     reset_launches();
-    if (!map || !h_pts || !d_pts_ws || !h_out || !d_ws) return TRI_EINVAL;
-    if (!map->diag || map->rho < 1) return TRI_EINVAL;
-    if (out_bytes < map->out_cells * 4u || (((uintptr_t)d_ws) & 31u)) return TRI_EINVAL;
+    if (!h_pts || !d_pts_ws || !h_out || !d_ws) return TRI_EINVAL;
+    // tri_edm's checks (map, strategy, rho, dim / ld, both capacities); RB has no band form
+    if (strategy == TRI_RB || edm_args_bad(map, strategy, dim, ld, pts_bytes, out_bytes)) return TRI_EINVAL;
+    if (pts_ws_bytes / 4u / (uint64_t)ld < (uint64_t)map->n || (((uintptr_t)d_pts_ws) & 15u)) return TRI_EINVAL;
+    if (((uintptr_t)d_ws) & 31u) return TRI_EINVAL;
+    if (map->out_cells == 0) return TRI_OK;
+    {   // one tile row of the slice (the band granule) must fit a workspace half and band_cells
+        const uint64_t half = (ws_bytes / 2 / 4) & ~7ull;
+        const uint64_t lim = band_cells && band_cells < half ? (band_cells & ~7ull) : half;
+        const uint64_t last = (uint64_t)map->row_end, first = last > (uint64_t)map->rho ? last - map->rho : 0;
+        if (T2(last) - T2(first) > lim) return TRI_EINVAL;
+    }
     uint64_t cap = (ws_bytes / 2 / 4) & ~7ull;          // floats per buffer, 32-byte multiple
     if (band_cells && band_cells < cap) cap = band_cells & ~7ull;
     const int64_t rho = map->rho;
@@ -313,7 +323,8 @@ extern "C" tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const
             cudaEventCreateWithFlags(&done_c[b], cudaEventDisableTiming) != cudaSuccess)
             rc = TRI_ECUDA;
     if (rc == TRI_OK &&
-        cudaMemcpyAsync(d_pts_ws, h_pts, (size_t)map->n * (size_t)ld * 4u, cudaMemcpyHostToDevice, sc) !=
+        cudaMemcpyAsync(d_pts_ws, h_pts, (size_t)(4ull * ((uint64_t)(map->n - 1) * (uint64_t)ld + (uint64_t)dim)),
+                        cudaMemcpyHostToDevice, sc) !=
             cudaSuccess)
         rc = TRI_ECUDA;
     int64_t ra = map->row_begin;

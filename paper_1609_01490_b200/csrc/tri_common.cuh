@@ -273,6 +273,10 @@ inline dim3 tile_grid(uint64_t nb) {
     return dim3((unsigned)gx, (unsigned)(gy ? gy : 1), 1);
 }
 
+// Shared argument validation of tri_edm / tri_edm_host (abi.cu): true = EINVAL.
+bool edm_args_bad(const tri_map_t *map, int32_t strategy, int32_t dim, int64_t ld, size_t pts_bytes,
+                  size_t out_bytes);
+
 // Kernel launchers (one per .cu file); args validated by abi.cu.
 tri_status launch_map_eval(uint64_t w0, uint64_t count, uint32_t *d_ij, unsigned long long *d_fail,
                            cudaStream_t st);
@@ -284,7 +288,10 @@ tri_status launch_tet_map_eval_lut(uint64_t w0, uint64_t count, uint32_t kmax, i
 tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
                                unsigned long long *d_first, cudaStream_t st);
 tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream_t st);
-tri_status launch_collide_tc(const tri_map_t &m, const float *sph, unsigned long long *count, cudaStream_t st);
+tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph, unsigned long long *count,
+                             void *ws, cudaStream_t st);
+size_t collide_tc_ws_bytes(const tri_map_t &m);
+tri_status launch_tc_tf32_probe(const float *x, const float *y, float *d, cudaStream_t st);
 tri_status launch_collide1d(const tri_map_t &m, int strategy, const float *iv, unsigned long long *count,
                             cudaStream_t st);
 tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,

@@ -116,8 +116,9 @@ def test_ca_steps_geometry_validation(L, rho, k, ok):
     m = tri.tri_map_init(1000, rho)
     if ok:
         return      # a valid pair would launch: covered by the GPU tests
-    rc = L.tri_ca_steps(ctypes.byref(m), 0, k, ctypes.c_void_p(1 << 20), ctypes.c_void_p(2 << 20), None, None,
-                        None, None)
+    big = m.out_cells
+    rc = L.tri_ca_steps(ctypes.byref(m), 0, k, ctypes.c_void_p(1 << 20), big, ctypes.c_void_p(2 << 20), big,
+                        None, 0, None, 0, None, None)
     assert rc == tri.TRI_EINVAL
 
 
@@ -129,7 +130,8 @@ def test_ca_steps_p2p_validation(L):
     vp = ctypes.c_void_p
     A, B, P = vp(1 << 20), vp(2 << 20), vp(3 << 20)
     m = tri.tri_map_init(1000, 128, 1, 1, 2, 1)
-    call = lambda mp, k, pa: L.tri_ca_steps_p2p(ctypes.byref(mp), 0, k, A, B, None, None, pa, None, None, None)
+    call = lambda mp, k, pa: L.tri_ca_steps_p2p(ctypes.byref(mp), 0, k, A, mp.out_cells, B, mp.out_cells,
+                                                None, 0, None, 0, pa, None, None, None)
     assert call(m, 4, vp((3 << 20) + 8)) == tri.TRI_EINVAL          # peer not 16-byte aligned
     assert call(m, 17, P) == tri.TRI_EINVAL                         # k > 16 at rho = 128
     small = tri.tri_map_init(230, 224, 1, 1, 2, 1)                  # rank 1 owns rows [224, 230)
@@ -149,8 +151,8 @@ def test_collide_rho384_is_tc_only(L):
     import ctypes
     m = tri.tri_map_init(1000, 384)
     for strat in (tri.TRI_LAMBDA, tri.TRI_BB, tri.TRI_LAMBDA_PERSIST):
-        assert L.tri_collide(ctypes.byref(m), strat, ctypes.c_void_p(1 << 20), ctypes.c_void_p(2 << 20),
-                             None) == tri.TRI_EINVAL
+        assert L.tri_collide(ctypes.byref(m), strat, ctypes.c_void_p(1 << 20), 16 * 1000,
+                             ctypes.c_void_p(2 << 20), 8, None, 0, None) == tri.TRI_EINVAL
 
 
 def test_host_lambda_vs_oracle(L, orc):
@@ -213,3 +215,93 @@ def test_tet_lut_bytes(L):
     assert L.tet_lut_build(511, 13, None, 0, None) == tri.TRI_EINVAL
     assert L.tet_lut_build(511, 13, 8, tri.tet_lut_bytes(511, 13) - 1, None) == tri.TRI_EINVAL
     assert L.tet_map_eval_lut(0, 10, 511, 13, None, None, 8, None) == tri.TRI_EINVAL
+
+
+# ---------------------------------------------------------------- capacities (include/tri.h conventions)
+def test_edm_host_validation(L):
+    """tri_edm_host runs tri_edm's checks before touching any buffer: a tile edge outside
+    {32, 64, 128, 256}, dim = 5, a short point workspace, a short band workspace, a
+    short host output, the RB strategy and a bad map all return EINVAL (fake pointers:
+    nothing is launched or copied)."""
+    import ctypes
+    vp = ctypes.c_void_p
+    n = 1000
+    H, D, O, W = vp(1 << 20), vp(1 << 24), vp(1 << 26), vp(1 << 28)
+
+    def call(m, strat=0, dim=3, pts_ws=4 * 3 * n, out=None, ws=1 << 24, band=0, pts=4 * 3 * n):
+        out = 4 * m.out_cells if out is None else out
+        return L.tri_edm_host(ctypes.byref(m), strat, H, dim, dim, pts, D, pts_ws, O, out, W, ws, band)
+
+    m16 = tri.tri_map_init(n, 16)
+    assert call(m16) == tri.TRI_EINVAL                                   # rho = 16: no EDM kernel
+    m = tri.tri_map_init(n, 128)
+    assert call(m, dim=5, pts=4 * 5 * n, pts_ws=4 * 5 * n) == tri.TRI_EINVAL   # dim outside 1..4
+    assert call(m, pts_ws=4 * 3 * n - 4) == tri.TRI_EINVAL               # point workspace one float short
+    assert call(m, pts=4 * 3 * n - 4) == tri.TRI_EINVAL                  # host points one float short
+    assert call(m, out=4 * m.out_cells - 1) == tri.TRI_EINVAL            # host output one byte short
+    assert call(m, ws=2 * 4 * 1000) == tri.TRI_EINVAL                    # a tile row (<= 128 000 cells) > a half
+    assert call(m, band=4096) == tri.TRI_EINVAL                          # ... or > band_cells
+    assert call(m, strat=tri.TRI_RB) == tri.TRI_EINVAL                   # RB has no band form
+    assert call(m, strat=99) == tri.TRI_EINVAL
+    bad = tri.tri_map_init(n, 128)
+    bad.m += 1                                                           # inconsistent descriptor
+    assert call(bad) == tri.TRI_EINVAL
+    ns = tri.tri_map_init(n, 128, 1, 0, 2, 0)                            # unsnapped multi-rank map
+    assert call(ns) == tri.TRI_EINVAL
+
+
+def test_edm_capacities(L):
+    import ctypes
+    vp = ctypes.c_void_p
+    m = tri.tri_map_init(1000, 128)
+    f = lambda pts, out, ld=3: L.tri_edm(ctypes.byref(m), 0, vp(1 << 20), 3, ld, pts, vp(1 << 24), out, None)
+    assert f(4 * 3 * 1000 - 4, 4 * m.out_cells) == tri.TRI_EINVAL
+    assert f(4 * 3 * 1000, 4 * m.out_cells - 4) == tri.TRI_EINVAL
+    assert f(4 * 4 * 1000 - 8, 4 * m.out_cells, ld=4) == tri.TRI_EINVAL   # strided rows: (n-1) ld + dim floats
+    m16 = tri.tri_map_init(1000, 16)
+    assert L.tri_edm(ctypes.byref(m16), 0, vp(1 << 20), 3, 3, 12000, vp(1 << 24), 4 * m16.out_cells,
+                     None) == tri.TRI_EINVAL
+
+
+def test_collide_triplet_ca_capacities(L):
+    """Short inputs / outputs are EINVAL before any launch (fake device pointers)."""
+    import ctypes
+    vp = ctypes.c_void_p
+    n = 1000
+    m = tri.tri_map_init(n, 256)
+    c = lambda sb, cb, strat=0, cnt=vp(2 << 20): L.tri_collide(ctypes.byref(m), strat, vp(1 << 20), sb, cnt, cb,
+                                                              None, 0, None)
+    assert c(16 * n - 16, 8) == tri.TRI_EINVAL                  # one sphere short
+    assert c(16 * n, 4) == tri.TRI_EINVAL                       # an int32 count
+    assert c(16 * n, 8, cnt=vp((2 << 20) + 4)) == tri.TRI_EINVAL  # count not 8-byte aligned
+    assert c(16 * n, 8, strat=tri.STRATEGIES["bb_tc"] + 1) == tri.TRI_EINVAL
+    # the tensor-core strategies need their workspace: m * rho * 64 bytes
+    mt = tri.tri_map_init(n, 384)
+    need = L.tri_collide_workspace_size(ctypes.byref(mt), 8)
+    assert need == mt.m * 384 * 64 and L.tri_collide_workspace_size(ctypes.byref(mt), 0) == 0
+    for strat in (8, 9):
+        assert L.tri_collide(ctypes.byref(mt), strat, vp(1 << 20), 16 * n, vp(2 << 20), 8, vp(3 << 20), need - 16,
+                             None) == tri.TRI_EINVAL
+        assert L.tri_collide(ctypes.byref(mt), strat, vp(1 << 20), 16 * n, vp(2 << 20), 8, None, need,
+                             None) == tri.TRI_EINVAL
+        assert L.tri_collide(ctypes.byref(mt), strat, vp(1 << 20), 16 * n, vp(2 << 20), 8, vp((3 << 20) + 8), need,
+                             None) == tri.TRI_EINVAL
+    assert L.tri_collide1d(ctypes.byref(m), 0, vp(1 << 20), 8 * n - 8, vp(2 << 20), 8, None) == tri.TRI_EINVAL
+    assert L.tri_collide1d(ctypes.byref(m), 0, vp(1 << 20), 8 * n, vp(2 << 20), 4, None) == tri.TRI_EINVAL
+    tm = tri.tet_map_init(64, 8)
+    t = lambda pb, eb: L.tet_triplet(ctypes.byref(tm), 0, vp(1 << 20), pb, 1.0, vp(2 << 20), eb, None)
+    assert t(16 * 63, 8 * 64) == tri.TRI_EINVAL
+    assert t(16 * 64, 8 * 63) == tri.TRI_EINVAL
+    mc = tri.tri_map_init(1000, 128, 1, 1, 2, 1)               # rank 1 of 2: both halos exist
+    R0, R1 = mc.row_begin, mc.row_end
+    assert R0 > 0 and R1 == 1000
+    oc = mc.out_cells
+    s1 = lambda ib, ob, ab: L.tri_ca_step(ctypes.byref(mc), 0, vp(1 << 20), ib, vp(1 << 24), ob, vp(1 << 26), ab,
+                                          None, 0, None, None)
+    assert s1(oc - 1, oc, R0) == tri.TRI_EINVAL
+    assert s1(oc, oc - 1, R0) == tri.TRI_EINVAL
+    assert s1(oc, oc, R0 - 1) == tri.TRI_EINVAL                 # the halo row above is R0 bytes
+    k = 4
+    sk = lambda ab: L.tri_ca_steps(ctypes.byref(mc), 0, k, vp(1 << 20), oc, vp(1 << 24), oc, vp(1 << 26), ab,
+                                   None, 0, None, None)
+    assert sk(T(R0) - T(R0 - k) - 1) == tri.TRI_EINVAL          # k rows above: T(R0) - T(R0 - k) bytes

@@ -317,26 +317,30 @@ def test_collide_knife_edge_pairs(orc, offset, scale):
             assert cnt.item() == ref, (rho, strategy)
 
 
+@pytest.mark.parametrize("strategy", ["tc", "bb_tc"])
 @pytest.mark.parametrize("rho", [256, 384, 512])
 @pytest.mark.parametrize("n,seed,rmax", [(1, 7, 0.1), (300, 42, 0.2), (1000, 42, 0.05), (5000, 7, 0.02),
-                                         (777, 42, 0.08)])
-def test_collide_tc_small(orc, n, seed, rmax, rho):
-    """TRI_LAMBDA_TC: the filter gap on the tensor cores (3xTF32 tcgen05), exact count."""
+                                         (777, 42, 0.08), (1153, 7, 0.3)])
+def test_collide_tc_small(orc, n, seed, rmax, rho, strategy):
+    """TRI_LAMBDA_TC / TRI_BB_TC: the filter on the tensor cores (one tcgen05 tf32 MMA per
+    128 x 128 block, TF32-exact operands), exact count."""
     s = inputs.spheres(n, seed, rmax)
     m = tri.tri_map_init(n, rho)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    tri.tri_collide(m, "tc", torch.from_numpy(s).cuda(), cnt)
+    tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
     sync()
     assert cnt.item() == orc.collide(s)
 
 
+@pytest.mark.parametrize("strategy", ["tc", "bb_tc"])
 @pytest.mark.parametrize("rho", [256, 384, 512])
-@pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (0.5, 1.0), (100.0, 1.0), (-1000.0, 10.0), (0.0, 1e-3)])
-def test_collide_tc_knife_edge(orc, offset, scale, rho):
+@pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (0.5, 1.0), (100.0, 1.0), (-1000.0, 10.0), (0.0, 1e-3),
+                                          (0.49, 1e-4), (3.0, 0.1)])
+def test_collide_tc_knife_edge(orc, offset, scale, rho, strategy):
     s = _near_touching(8192, 11, offset, scale)
     m = tri.tri_map_init(len(s), rho)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    tri.tri_collide(m, "tc", torch.from_numpy(s).cuda(), cnt)
+    tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
     sync()
     assert cnt.item() == orc.collide(s)
 

@@ -1,0 +1,122 @@
+"""GPU tests of the tensor-core collision filter (-m gpu): the hardware accumulation
+bound its margin assumes, and exact counts on inputs built to defeat a filter
+(csrc/collide_tc.cu header; reading Q9)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1609_01490_b200 import inputs  # noqa: E402
+from paper_1609_01490_b200 import tri  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    tri.lib()
+
+
+def tf32(a):
+    """Truncate fp32 values to TF32 (low 13 mantissa bits cleared): exact TF32 operands."""
+    a = np.ascontiguousarray(a, np.float32)
+    return (a.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+def probe(X, Y):
+    d = torch.empty((128, 128), dtype=torch.float32, device="cuda")
+    tri.tri_tc_tf32_probe(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), d)
+    torch.cuda.synchronize()
+    return d.cpu().numpy().astype(np.float64)
+
+
+def exact(X, Y):
+    """Exact X Y^T: TF32 x TF32 products have <= 22 significant bits and the 8-term sums
+    of these operands stay far inside fp64's 53 bits (checked by the exponent span)."""
+    Xd, Yd = X.astype(np.float64), Y.astype(np.float64)
+    terms = Xd[:, None, :] * Yd[None, :, :]
+    return terms.sum(-1), np.abs(terms).sum(-1)
+
+
+def cancelling_operands(seed, scale, jitter):
+    """Rows x_i and columns y_j = x_i' + tiny, in the filter's form
+    X = (x, P_hi, P_lo, 1, 1, 0), Y = (-2y, 1, 1, Q_hi, Q_lo, 0) with P = |x|^2, Q = |y|^2:
+    X.Y = |x - y|^2 (+ split residue), the largest cancellation the filter meets."""
+    rng = np.random.default_rng(seed)
+    x = tf32(rng.uniform(-scale, scale, (128, 3)))
+    y = tf32(x[rng.permutation(128)] + rng.normal(0, jitter * scale, (128, 3)))
+    y[:64] = x[:64]                                   # and some exactly coincident pairs
+    X = np.zeros((128, 8), np.float32)
+    Y = np.zeros((128, 8), np.float32)
+    P = (x.astype(np.float64) ** 2).sum(1)
+    Q = (y.astype(np.float64) ** 2).sum(1)
+    Ph = tf32(P.astype(np.float32)); Pl = tf32((P - Ph).astype(np.float32))
+    Qh = tf32(Q.astype(np.float32)); Ql = tf32((Q - Qh).astype(np.float32))
+    X[:, :3], X[:, 3], X[:, 4], X[:, 5], X[:, 6] = x, Ph, Pl, 1, 1
+    Y[:, :3], Y[:, 3], Y[:, 4], Y[:, 5], Y[:, 6] = tf32(-2 * y), 1, 1, Qh, Ql
+    return tf32(X), tf32(Y)
+
+
+@pytest.mark.parametrize("case", ["random", "cancel_unit", "cancel_large", "cancel_tiny", "mixed_exponents"])
+def test_tc_tf32_accumulation_bound(case):
+    """The filter's margin assumes |fp32 tensor-core sum - exact sum| <= 2^-20 sum |x_k y_k|
+    for one K = 8 tf32 MMA into a zeroed accumulator (csrc/collide_tc.cu).  Measured here
+    on random and on maximally cancelling operands; the observed worst case is reported."""
+    rng = np.random.default_rng(3)
+    if case == "random":
+        X, Y = tf32(rng.uniform(-1, 1, (128, 8))), tf32(rng.uniform(-1, 1, (128, 8)))
+    elif case == "cancel_unit":
+        X, Y = cancelling_operands(5, 0.5, 1e-3)
+    elif case == "cancel_large":
+        X, Y = cancelling_operands(6, 1000.0, 1e-6)
+    elif case == "cancel_tiny":
+        X, Y = cancelling_operands(7, 1e-3, 1e-2)
+    else:
+        e = rng.integers(-20, 20, (128, 8))
+        X = tf32(rng.uniform(1, 2, (128, 8)) * np.exp2(e) * rng.choice([-1, 1], (128, 8)))
+        Y = tf32(rng.uniform(1, 2, (128, 8)) * np.exp2(-e[rng.permutation(128)]) * rng.choice([-1, 1], (128, 8)))
+    d = probe(X, Y)
+    ex, ab = exact(X, Y)
+    err = np.abs(d - ex)
+    ratio = float((err / np.maximum(ab, 1e-300)).max())
+    print(f"{case}: max |err| / sum|terms| = {ratio:.3e} (bound 2^-20 = {2.0 ** -20:.3e})")
+    assert np.all(err <= 2.0 ** -20 * ab), ratio
+
+
+@pytest.mark.parametrize("strategy,rho", [("tc", 384), ("bb_tc", 256), ("tc", 512)])
+def test_collide_tc_special_values(orc, strategy, rho):
+    """NaN, infinite and huge coordinates or radii never break exactness: the filter
+    treats them as never- or always-flagged and the exact predicate decides."""
+    s = inputs.spheres(3000, 9, 0.05)
+    s[10] = [np.nan, 0.5, 0.5, 0.01]
+    s[20, 3] = np.nan
+    s[30] = [np.inf, 0.2, 0.2, 0.01]
+    s[40] = [1e20, 1e20, 0.0, 0.01]
+    s[41] = [1e20, 1e20, 0.0, 0.01]                    # coincident with 40: counted in fp32
+    s[50, 3] = 3.0                                     # a huge sphere overlapping most others
+    s[2990] = s[5]                                     # an exactly coincident pair, far apart in index
+    s[2991, :3] = s[6, :3]
+    s[2991, 3] = 0.0                                   # zero radius inside a sphere
+    m = tri.tri_map_init(len(s), rho)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
+    torch.cuda.synchronize()
+    assert cnt.item() == orc.collide(s)
+
+
+@pytest.mark.parametrize("strategy", ["tc", "bb_tc"])
+def test_collide_tc_dense_cluster(orc, strategy):
+    """Every pair of a dense cluster collides (every group flagged, every column recounted):
+    the count is C(n, 2) on the diagonal and off-diagonal tiles alike."""
+    n = 1500
+    rng = np.random.default_rng(4)
+    s = np.zeros((n, 4), np.float32)
+    s[:, :3] = 0.3 + rng.random((n, 3)) * 1e-3
+    s[:, 3] = 0.01
+    m = tri.tri_map_init(n, 384)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
+    torch.cuda.synchronize()
+    assert cnt.item() == orc.collide(s) == n * (n - 1) // 2
