@@ -231,7 +231,9 @@ def bench_edm(args, rank, world, local_rank, pk):
     for s in ("bb", "lambda", "persist", "clc") + (("rb",) if world == 1 else ()):
         t, _ = time_steps(lambda s=s: tri.tri_edm(m, s, pts, out), Kc, 2, world)
         vs[s + "_ms"] = round(max_over_ranks(t, world) / Kc, 4)
-    vs["I_lambda"] = round(vs["bb_ms"] / vs["lambda_ms"], 4)
+    vs["I_lambda_single"] = round(vs["bb_ms"] / vs["lambda_ms"], 4)
+    if world == 1:
+        vs["I_lambda"] = ratio_stats(lambda: tri.tri_edm(m, "bb", pts, out), lambda: tri.tri_edm(m, "lambda", pts, out))
     vs["I_persist"] = round(vs["bb_ms"] / vs["persist_ms"], 4)
     vs["I_clc"] = round(vs["bb_ms"] / vs["clc_ms"], 4)          # persistent CTAs, cluster launch control
     if "rb_ms" in vs:
@@ -265,6 +267,51 @@ def bench_edm(args, rank, world, local_rank, pk):
             "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)), "map": m.as_dict()}
 
 
+# ----------------------------------------------------------------------------- helpers
+def ratio_stats(run_bb, run_lam, reps=11):
+    """Like-for-like lambda vs BB (I = t_BB / t_lambda): `reps` alternating
+    timings of each, one launch plan per timing (CUDA events, after a warm-up of both);
+    I per repetition, reported as median with min / max."""
+    import torch
+    for f in (run_bb, run_lam):
+        f()
+    torch.cuda.synchronize()
+    tb, tl, r = [], [], []
+    for _ in range(reps):
+        out = []
+        for f in (run_bb, run_lam):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f()
+            e1.record()
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        tb.append(out[0])
+        tl.append(out[1])
+        r.append(out[0] / out[1])
+    med = statistics.median
+    return {"I": round(med(r), 4), "I_min": round(min(r), 4), "I_max": round(max(r), 4), "reps": reps,
+            "bb_ms": round(med(tb), 4), "lambda_ms": round(med(tl), 4)}
+
+
+def fp32_peak(pk):
+    return 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e12        # FP32 lane-ops / s (TFLOP/s), B200_PROFILING.md
+
+
+def tf32_peak(pk):
+    return pk["bf16_tflops"] / 2.0                          # measured bf16 x nominal tf32 : bf16 = 1 : 2
+
+
+def ncu_metric(name, key):
+    """A per-launch counter of the committed ncu --set full summary (profiles/ncu_summary.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(name, {}).get(key)
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------- other configs
 def bench_dummy(pk):
     import torch
@@ -276,8 +323,11 @@ def bench_dummy(pk):
     for s in ("bb", "lambda", "persist", "rb"):
         us = 1e3 * graph_time(lambda s=s: tri.tri_dummy(m, s, tri.TRI_DUMMY_PACKED, out), 100)
         res[s + "_us"] = round(us, 3)
+    # like-for-like: graphs of 100 launches, 11 alternating repetitions
+    gb = _graph(lambda: tri.tri_dummy(m, "bb", tri.TRI_DUMMY_PACKED, out), 100)
+    gl = _graph(lambda: tri.tri_dummy(m, "lambda", tri.TRI_DUMMY_PACKED, out), 100)
+    res["I_lambda"] = ratio_stats(gb.replay, gl.replay)
     res["I_rb"] = round(res["bb_us"] / res["rb_us"], 4)
-    res["I_lambda"] = round(res["bb_us"] / res["lambda_us"], 4)
     res["I_persist"] = round(res["bb_us"] / res["persist_us"], 4)
     # section 4.1 / Fig. 2 on B200: the paper's uncorrected sqrt variants vs BB, and
     # the first omega each variant gets wrong (GPU validity scan over omega < 2^26)
@@ -291,12 +341,14 @@ def bench_dummy(pk):
         sq[name] = {"us": round(us, 3), "I": round(res["bb_us"] / us, 4),
                     "first_wrong_omega": int(first.item()) if fail.item() else None,
                     "wrong_below_2^26": int(fail.item())}
-    sq["lambda (rsqrt + integer correction)"] = {"us": res["lambda_us"], "I": res["I_lambda"],
-                                                 "first_wrong_omega": None, "exact_to": "2^40"}
+    sq["lambda (rsqrt + integer correction)"] = {"us": res["lambda_us"], "first_wrong_omega": None,
+                                                 "exact_to": "2^40"}
     res["sqrt_variants"] = sq
     res["cells_per_s"] = T(n) / (min(res["lambda_us"], res["persist_us"]) * 1e-6)
     res["ctas"] = {"lambda": m.blocks, "bb": m.m * m.m}
     res["wasted_threads"] = {"lambda": m.waste_lambda, "bb": m.waste_bb}
+    res["roofline"] = {"bound": "launch", "note": "n = 2048: 8.39 MB of codes (L2-resident); the cost is "
+                       "CTA dispatch -- 8,256 lambda tiles vs 16,384 BB tiles"}
     # bandwidth point: n = 65536 packed codes (8.59 GB)
     n2 = 65536
     m2 = tri.tri_map_init(n2, rho)
@@ -304,7 +356,8 @@ def bench_dummy(pk):
     for s in ("bb", "lambda", "persist", "rb"):
         t, _ = time_steps(lambda s=s: tri.tri_dummy(m2, s, tri.TRI_DUMMY_PACKED, out2), 5, 2, 1)
         res[f"n65536_{s}_ms"] = round(t / 5, 4)
-    res["n65536_I"] = round(res["n65536_bb_ms"] / res["n65536_lambda_ms"], 4)
+    res["n65536_I"] = ratio_stats(lambda: tri.tri_dummy(m2, "bb", tri.TRI_DUMMY_PACKED, out2),
+                                  lambda: tri.tri_dummy(m2, "lambda", tri.TRI_DUMMY_PACKED, out2))
     res["n65536_I_persist"] = round(res["n65536_bb_ms"] / res["n65536_persist_ms"], 4)
     res["n65536_I_rb"] = round(res["n65536_bb_ms"] / res["n65536_rb_ms"], 4)
     best2 = min(res["n65536_lambda_ms"], res["n65536_persist_ms"])
@@ -312,9 +365,45 @@ def bench_dummy(pk):
     res["n65536_frac"] = round(res["n65536_GBps"] / pk["hbm_gbs"], 4)
     res["n65536_note"] = ("the paper's one-thread-per-cell form (4-byte stores, rho x rho threads): it "
                           "measures the map's cost, not the write ceiling; the same 8.59 GB packed "
-                          "write with aligned 16-byte chunk stores is the EDM headline (>= 92 % of peak)")
+                          "write with aligned 16-byte chunk stores is the EDM headline")
     return {"config": "dummy map-cost kernel, n=2048, rho=16 (PACKED u32 codes)", "metric": "cells/s",
             "value": res["cells_per_s"], **res}
+
+
+def _graph(step, reps):
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            step()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            step()
+    return g
+
+
+def bench_edm4(pk):
+    """The paper's own EDM workload shape (4 features per point), n = 65536."""
+    import torch
+    from paper_1609_01490_b200 import inputs, tri
+    n = EDM_N
+    pts = torch.from_numpy(inputs.points(n, 4, 42)).cuda()
+    m = tri.tri_map_init(n, EDM_RHO)
+    out = torch.empty(m.out_cells, dtype=torch.float32, device="cuda")
+    t, _ = time_steps(lambda: tri.tri_edm(m, "lambda", pts, out), 20, 3, 1)
+    ms = t / 20
+    gbs = (4 * m.out_cells + 16 * n) / (ms * 1e-3) / 1e9
+    I = ratio_stats(lambda: tri.tri_edm(m, "bb", pts, out), lambda: tri.tri_edm(m, "lambda", pts, out))
+    return {"config": "EDM n=65536, 4 features per point (P:486-487), packed triangular output",
+            "metric": "cells/s", "value": T(n) / (ms * 1e-3), "ms": round(ms, 4), "I_lambda": I,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(gbs / pk["hbm_gbs"], 4), "bytes_per_cell": 4}}
+
+
+COLLIDE_TC_RHO = 1024          # the tcgen05 kernel's best tile edge on B200 (256 ... 1024 measured)
 
 
 def bench_collide(rank, world, pk):
@@ -323,61 +412,75 @@ def bench_collide(rank, world, pk):
     n, rho = 200000, 256
     s = torch.from_numpy(inputs.spheres(n, 42)).cuda()
     m = tri.tri_map_init(n, rho, 1, rank, world, 0)
+    m_tc = tri.tri_map_init(n, COLLIDE_TC_RHO, 1, rank, world, 0)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     res = {}
-    for st in ("bb", "persist", "lambda"):
-        def step(st=st):
-            tri.tri_collide(m, st, s, cnt)
+    for st, mm in (("bb", m), ("persist", m), ("lambda", m), ("bb_tc", m_tc), ("tc", m_tc)):
+        def step(st=st, mm=mm):
+            tri.tri_collide(mm, st, s, cnt)
             tdist.allreduce_count(cnt)
         t, _ = time_steps(step, 3, 1, world)
         res[st + "_ms"] = round(max_over_ranks(t, world) / 3, 4)
         res[st + "_count"] = int(cnt.item())
-    # the experimental tensor-core filter (TRI_LAMBDA_TC: 3xTF32 mma.sync), for comparison
-    m_tc = tri.tri_map_init(n, 384, 1, rank, world, 0)          # the tcgen05 kernel's best tile edge
-    def step_tc():
-        tri.tri_collide(m_tc, "tc", s, cnt)
-        tdist.allreduce_count(cnt)
-    t, _ = time_steps(step_tc, 3, 1, world)
-    res["tc_ms"] = round(max_over_ranks(t, world) / 3, 4)
-    res["tc_count"] = int(cnt.item())
     pairs = n * (n - 1) // 2
-    simt = min(res["persist_ms"], res["lambda_ms"])
-    best = min(simt, res["tc_ms"]) if res["tc_count"] == res["lambda_count"] else simt
-    res["best"] = "tc" if best == res.get("tc_ms") else ("lambda" if best == res["lambda_ms"] else "persist")
-    res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
-    res["I_persist"] = round(res["bb_ms"] / res["persist_ms"], 4)
-    res["I_tc"] = round(res["bb_ms"] / res["tc_ms"], 4)
-    # SIMT roofline: the hot loop's 5 fma-pipe ops per pair (the 4-D dot-product filter:
-    # 4 FFMA + 1 FADD, packed f32x2) on 128 lanes/SM; the exact 9-op predicate runs only
-    # on flagged (row, column) pairs (~7e-6 of them)
-    peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
-    ach = 5.0 * pairs / world / (simt * 1e-3) / 1e12
-    simt_roof = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "TFLOP/s (fp32 ops)",
-                 "frac": round(ach / peak, 4), "ops_per_pair": 5, "kernel": "collide_kernel<256> (SIMT filter)",
-                 "note": "filter ops; the exact predicate (9 ops) runs on flagged pairs only"}
-    # tensor roofline of the tcgen05 filter: 3 kind::tf32 MMAs (3xTF32 split) with K = 8
-    # per pair = 48 executed TF32 flops per pair, against the TF32 dense peak (the measured
-    # bf16 cuBLAS peak x the nominal tf32 : bf16 ratio 1 : 2)
-    tpeak = pk["bf16_tflops"] / 2.0
-    tach = 48.0 * pairs / world / (res["tc_ms"] * 1e-3) / 1e12
-    tc_roof = {"bound": "tensor", "achieved": round(tach, 1), "peak": round(tpeak, 1), "unit": "TFLOP/s (tf32)",
-               "frac": round(tach / tpeak, 4), "flops_per_pair": 48, "kernel": "collide_tc_kernel (tcgen05)",
-               "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (nominal tf32 rate)"}
-    res["roofline"] = tc_roof if res["best"] == "tc" else simt_roof
-    res["roofline_simt"] = simt_roof
-    res["roofline_tc"] = tc_roof
+    counts = {res[k] for k in res if k.endswith("_count")}
+    assert len(counts) == 1, f"strategies disagree on the count: {res}"
+    best = res["tc_ms"]
+    res["best"] = "tc"
+    res["rho_simt"], res["rho_tc"] = rho, COLLIDE_TC_RHO
+    if world == 1:
+        # like-for-like improvement factors: the same tile body on the lambda and BB grids
+        res["I_lambda_tc"] = ratio_stats(lambda: tri.tri_collide(m_tc, "bb_tc", s, cnt),
+                                         lambda: tri.tri_collide(m_tc, "tc", s, cnt))
+        res["I_lambda_simt"] = ratio_stats(lambda: tri.tri_collide(m, "bb", s, cnt),
+                                           lambda: tri.tri_collide(m, "lambda", s, cnt))
+    res["I_persist_simt"] = round(res["bb_ms"] / res["persist_ms"], 4)
+    sec = best * 1e-3
+    clk = pk["sm_max_mhz"] * 1e6
+    # rooflines in the method's units: the pair test is ~10 FP32 ops (3 FADD,
+    # FMUL, 2 FFMA, FADD, FMUL, FSETP, IADD); as a contraction its minimum is ONE K = 6 dot
+    # product (x, y, z, r, A, 1) = 12 flops.  The tcgen05 kernel executes K = 8 (16 flops).
+    res["roofline"] = {"bound": "tensor", "achieved": round(12.0 * pairs / world / sec / 1e12, 1),
+                       "peak": round(tf32_peak(pk), 1), "unit": "TFLOP/s (tf32)",
+                       "frac": round(12.0 * pairs / world / sec / 1e12 / tf32_peak(pk), 4),
+                       "flops_per_pair": 12, "executed_flops_per_pair": 16,
+                       "kernel": f"collide_tc_kernel<{COLLIDE_TC_RHO}, lambda> (tcgen05)",
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (nominal tf32 : bf16)"}
+    res["roofline_method_alu"] = {"bound": "alu", "achieved": round(10.0 * pairs / world / sec / 1e12, 2),
+                                  "peak": round(fp32_peak(pk), 2), "unit": "TFLOP/s (fp32 ops)",
+                                  "frac": round(10.0 * pairs / world / sec / 1e12 / fp32_peak(pk), 4),
+                                  "ops_per_pair": 10,
+                                  "note": "the SIMT formulation's work: > 1 means the tensor cores do it"}
+    # what the tcgen05 kernel's epilogue actually spends per pair: 4 B of TMEM read, and
+    # half a 3-input LOP3 (two sign bits per ALU op, 64 ALU lanes per SM per clock)
+    tm = 4.0 * pairs / world / sec / 1e12
+    tm_peak = 950.0 * 148 * clk / 1e12
+    res["roofline_tmem"] = {"bound": "tmem", "achieved": round(tm, 1), "peak": round(tm_peak, 1), "unit": "TB/s",
+                            "frac": round(tm / tm_peak, 4), "bytes_per_pair": 4,
+                            "peak_source": "tools/probes/tmem_bw.cu: 950 B/clk/SM measured on B200"}
+    al = 0.5 * pairs / world / sec
+    al_peak = 148 * 64 * clk
+    res["roofline_epilogue_alu"] = {"bound": "alu", "achieved": round(al / 1e12, 2), "peak": round(al_peak / 1e12, 2),
+                                    "unit": "T LOP3/s", "frac": round(al / al_peak, 4), "ops_per_pair": 0.5}
+    simt = min(res["lambda_ms"], res["persist_ms"])
+    res["roofline_simt"] = {"bound": "alu", "achieved": round(5.0 * pairs / world / (simt * 1e-3) / 1e12, 2),
+                            "peak": round(fp32_peak(pk), 2), "unit": "TFLOP/s (fp32 ops)",
+                            "frac": round(5.0 * pairs / world / (simt * 1e-3) / 1e12 / fp32_peak(pk), 4),
+                            "ops_per_pair": 5, "kernel": "collide_kernel<256> (SIMT 4-D dot-product filter)"}
     return {"config": "collision count, n=200000 spheres, r~U[0,0.01)", "metric": "pair tests/s",
-            "value": pairs / (best * 1e-3), **res}
+            "value": pairs / sec, **res}
 
 
-def bench_ca(rank, world, pk, steps=100):
+CA_RHO1, CA_RHOK, CA_K = 128, 224, 8     # tile edges: tri_ca_step (k = 1) and tri_ca_steps; generations per launch
+
+
+def bench_ca(rank, world, pk, clocks=None, steps=100):
     import torch
     from paper_1609_01490_b200 import dist as tdist, inputs, tri
     n = 32768
-    RHO1, RHOK = 128, 224          # tile edges: tri_ca_step (k = 1) and tri_ca_steps (the faster geometry for each)
-    K = 8                                              # generations per tri_ca_steps launch (deep halos)
     st = inputs.ca_state(n, 42)
     full = torch.from_numpy(st)
+    K = CA_K
     plan = [K] * (steps // K) + ([steps % K] if steps % K else [])
 
     def setup(rho, ks):
@@ -394,36 +497,48 @@ def bench_ca(rank, world, pk, steps=100):
 
     res = {}
     # single-generation kernel (tri_ca_step, one halo row each side every step)
-    m, bounds, bufs, halo = setup(RHO1, {1})
-    cells1 = m.out_cells
+    m1, bounds1, bufs1, halo1 = setup(CA_RHO1, {1})
+
+    def run1(strat):
+        x, y = bufs1
+        above, below = halo1[1]
+        for _ in range(steps):
+            if world > 1:
+                tdist.halo_exchange(x, bounds1, n, rank, above, below)
+            tri.tri_ca_step(m1, strat, x, y, above, below)
+            x, y = y, x
     for strat in ("bb", "persist", "lambda"):
-        def run(strat=strat):
-            x, y = bufs
-            above, below = halo[1]
-            for _ in range(steps):
-                if world > 1:
-                    tdist.halo_exchange(x, bounds, n, rank, above, below)
-                tri.tri_ca_step(m, strat, x, y, above, below)
-                x, y = y, x
-        t, _ = time_steps(run, 1, 1, world)
+        t, _ = time_steps(lambda strat=strat: run1(strat), 1, 1, world)
         res["step_" + strat + "_ms"] = round(max_over_ranks(t, world), 3)
     # K generations per launch (tri_ca_steps, K-row halos every K steps)
-    m, bounds, bufs, halo = setup(RHOK, set(plan))
-    for strat in ("bb", "lambda"):
-        def run(strat=strat):
-            x, y = bufs
-            for k in plan:
-                above, below = halo[k]
-                if world > 1:
-                    tdist.halo_exchange(x, bounds, n, rank, above, below, k)
+    m, bounds, bufs, halo = setup(CA_RHOK, set(plan))
+
+    def runk(strat, exchange=True, compute=True):
+        x, y = bufs
+        for k in plan:
+            above, below = halo[k]
+            if world > 1 and exchange:
+                tdist.halo_exchange(x, bounds, n, rank, above, below, k)
+            if compute:
                 tri.tri_ca_steps(m, strat, k, x, y, above, below)
-                x, y = y, x
-        t, _ = time_steps(run, 1, 1, world)
+            x, y = y, x
+    for strat in ("bb", "lambda"):
+        t, _ = time_steps(lambda strat=strat: runk(strat), 1, 1, world)
         res[strat + "_ms"] = round(max_over_ranks(t, world), 3)
-    res["rho_single_step"], res["rho_k_steps"] = RHO1, RHOK
+    if world == 1:
+        res["I_lambda"] = ratio_stats(lambda: runk("bb"), lambda: runk("lambda"))
+        res["I_lambda_single_step"] = ratio_stats(lambda: run1("bb"), lambda: run1("lambda"))
+    else:
+        # the halo exchange alone (NCCL send/recv of the K-row halos, same plan), shown separately
+        t, _ = time_steps(lambda: runk("lambda", compute=False), 1, 1, world)
+        res["halo_exchange_ms"] = round(max_over_ranks(t, world), 3)
+        t, _ = time_steps(lambda: runk("lambda", exchange=False), 1, 1, world)
+        res["compute_only_ms"] = round(max_over_ranks(t, world), 3)
+    res["rho_single_step"], res["rho_k_steps"] = CA_RHO1, CA_RHOK
     if world > 1:
         # the same plan with the halo exchange fused into the kernel's stores (CUDA IPC
-        # peer memory over NVLink, one stream-ordered 4-byte all-reduce per launch)
+        # peer memory over NVLink, a system-scope release per launch + one stream-ordered
+        # 4-byte all-reduce per launch)
         try:
             h = tdist.P2PHalo(bounds, n, rank, K)
             R0, R1 = bounds[rank]
@@ -449,18 +564,29 @@ def bench_ca(rank, world, pk, steps=100):
         except Exception as ex:  # noqa: BLE001 -- reported, the NCCL-exchange number stands
             res["p2p_error"] = repr(ex)[:200]
     best = res["lambda_ms"]
-    res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
-    res["I_lambda_single_step"] = round(res["step_bb_ms"] / res["step_lambda_ms"], 4)
     res["generations_per_launch"] = K
     cells = T(n) * steps
-    # per launch the kernel reads + writes each cell once: 2 B/cell per K generations
     launches = len(plan)
+    # HBM: per launch the kernel reads + writes each cell once: 2 B/cell per K generations
     gbs = 2 * (m.out_cells * launches) / (best * 1e-3) / 1e9
-    gbs1 = 2 * (cells1 * steps) / (res["step_lambda_ms"] * 1e-3) / 1e9
+    gbs1 = 2 * (m1.out_cells * steps) / (res["step_lambda_ms"] * 1e-3) / 1e9
     res["roofline"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                        "frac": round(gbs / pk["hbm_gbs"], 4), "bytes_per_cell_generation": round(2 / K, 3),
-                       "note": f"tri_ca_steps, {K} generations per launch; the single-step kernel reaches "
-                               f"{round(gbs1, 1)} GB/s ({round(gbs1 / pk['hbm_gbs'], 4)} of peak) at 2 B/cell"}
+                       "note": f"tri_ca_steps, {K} generations per launch: not HBM-bound (issue-bound, see "
+                               f"roofline_issue); the single-step kernel reaches {round(gbs1, 1)} GB/s "
+                               f"({round(gbs1 / pk['hbm_gbs'], 4)} of peak) at 2 B/cell"}
+    # instruction roofline of the k = 8 kernel: SASS warp-instructions per launch (ncu,
+    # profiles/ncu_summary.json) over the measured per-launch time vs the issue peak
+    inst = ncu_metric("ca_multi", "inst_per_launch")
+    if inst:
+        mhz = (clocks or {}).get("sm_mhz") or pk["sm_max_mhz"]
+        per_launch = best * 1e-3 / launches
+        ach = inst / per_launch
+        peak = 148 * 4 * mhz * 1e6
+        res["roofline_issue"] = {"bound": "issue", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
+                                 "unit": "T warp-instr/s", "frac": round(ach / peak, 4),
+                                 "inst_per_cell_generation": round(inst * 32 / (m.out_cells * K), 3),
+                                 "note": "4 schedulers x 1 warp-instruction / clock / SM at the run's median SM clock"}
     return {"config": f"triangular Life B3/S23, n=32768, {steps} generations", "metric": "cell-updates/s",
             "value": cells / (best * 1e-3), **res}
 
@@ -481,16 +607,17 @@ def bench_collide1d(rank, world, pk):
         t, _ = time_steps(step, 3, 1, world)
         res[st + "_ms"] = round(max_over_ranks(t, world) / 3, 4)
         res[st + "_count"] = int(cnt.item())
-    res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
+    if world == 1:
+        res["I_lambda"] = ratio_stats(lambda: tri.tri_collide1d(m, "bb", iv, cnt),
+                                      lambda: tri.tri_collide1d(m, "lambda", iv, cnt))
     pairs = n * (n - 1) // 2
     # the hot loop's filter per pair: one packed FADD2 (2 FP32 lane-ops, FMA pipe, 128 lanes/SM/clk)
     # and one LOP3 (ALU pipe, 64 lanes/SM/clk) -- both pipes bound at the same pair rate,
     # 148 x 64 pairs/clk; reported as the FP32 ops (2 per pair) against the FP32 peak
     ops = 2.0 * pairs / world
-    peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
     ach = ops / (res["lambda_ms"] * 1e-3) / 1e12
-    res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2),
-                       "unit": "TFLOP/s (fp32 ops)", "frac": round(ach / peak, 4), "ops_per_pair": 2,
+    res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(fp32_peak(pk), 2),
+                       "unit": "TFLOP/s (fp32 ops)", "frac": round(ach / fp32_peak(pk), 4), "ops_per_pair": 2,
                        "note": "filter: FADD2 + LOP3 per pair; the exact predicate runs on flagged pairs only"}
     return {"config": "1-D collision count, n=200000 intervals, r~U[0,1e-5)", "metric": "pair tests/s",
             "value": pairs / (res["lambda_ms"] * 1e-3), **res}
@@ -503,10 +630,12 @@ def bench_triplet(rank, world, pk):
     x = torch.from_numpy(inputs.points4(n, 42)).cuda()
     e = torch.empty(n, dtype=torch.float64, device="cuda")
     res = {}
+    maps = {}
     for strat, rho in (("bb", 32), ("persist", 32), ("lambda", 32)):
         tm = tri.tet_map_init(n, rho, rank, world) if strat != "bb" else tri.tet_map_init(n, rho)
         if strat == "bb" and world > 1:
             continue
+        maps[strat] = tm
 
         def step(tm=tm, strat=strat):
             tri.tet_triplet(tm, strat, x, e)
@@ -514,17 +643,20 @@ def bench_triplet(rank, world, pk):
         t, _ = time_steps(step, 3, 1, world)
         res[strat + "_ms"] = round(max_over_ranks(t, world) / 3, 4)
     best = min(res["persist_ms"], res["lambda_ms"])
-    if "bb_ms" in res:
-        res["I_lambda"] = round(res["bb_ms"] / res["lambda_ms"], 4)
+    if world == 1:
+        res["I_lambda"] = ratio_stats(lambda: tri.tet_triplet(maps["bb"], "bb", x, e),
+                                      lambda: tri.tet_triplet(maps["lambda"], "lambda", x, e))
         res["I_persist"] = round(res["bb_ms"] / res["persist_ms"], 4)
     trip = n * (n - 1) * (n - 2) // 6
     # FP32 ops per triplet in the f32x2 formulation: 10 for E = r^3 (1 + P' r^2) from
-    # (a, b, c) plus 2 FMAs folding E into the e_s and row (e_p, e_q) accumulators; +1 MUFU.RSQ
+    # (a, b, c) plus 2 FMAs folding E into the e_s and row (e_p, e_q) accumulators; +1 MUFU.RSQ.
+    # (SURVEY 8(d) estimated ~20 FP32 + 2 MUFU: the algebraic form needs fewer.)
     ops = 12.0 * trip / world
-    peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
     ach = ops / (best * 1e-3) / 1e12
-    res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "TFLOP/s (fp32 ops)",
-                       "frac": round(ach / peak, 4), "ops_per_triplet": 12, "mufu_per_triplet": 1}
+    res["roofline"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(fp32_peak(pk), 2),
+                       "unit": "TFLOP/s (fp32 ops)", "frac": round(ach / fp32_peak(pk), 4), "ops_per_triplet": 12,
+                       "mufu_per_triplet": 1, "survey_estimate_ops_per_triplet": 20,
+                       "frac_at_survey_estimate": round(20.0 * trip / world / (best * 1e-3) / 1e12 / fp32_peak(pk), 4)}
     res["tiles"] = {"tet": tri.tet_map_init(n, 32).blocks, "bb3d": 128 ** 3}
     # succinct lookup table vs cube root for the tetrahedral layer: map evaluations
     # per second (two maps + the Eq./successor checks per omega) over every tile of n = 4096 at
@@ -545,6 +677,76 @@ def bench_triplet(rank, world, pk):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _timed(fn, target_s):
+    """Run fn (one bounded oracle sample) repeatedly for about target_s; (calls, seconds)."""
+    t0 = time.perf_counter()
+    fn()
+    dt = time.perf_counter() - t0
+    reps = max(1, min(100, int(target_s / max(dt, 1e-4))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    return reps, time.perf_counter() - t0
+
+
+def cpu_baseline_of(fn, units, unit, desc, target_s=3.0):
+    """The oracle as it stands, timed on a bounded sample on all host cores and on one core
+    (SURVEY 8(d)): {"value": units/s all cores, "value_1core": units/s one core, ...}."""
+    import oracle
+    oracle.set_threads(0)
+    cores = oracle.num_threads()
+    reps, dt = _timed(fn, target_s)
+    oracle.set_threads(1)
+    reps1, dt1 = _timed(fn, target_s)
+    oracle.set_threads(0)
+    return {"value": units * reps / dt, "unit": unit, "cores": cores, "kind": "oracle",
+            "value_1core": units * reps1 / dt1, "cpu_model": cpu_model(),
+            "sample": f"{desc}; {reps} x in {dt:.2f} s on {cores} threads, {reps1} x in {dt1:.2f} s on 1"}
+
+
+def cpu_baselines():
+    """One bounded oracle sample per BASELINE config (rank 0, N = 1 only)."""
+    import oracle
+    from paper_1609_01490_b200 import inputs
+    out = {}
+    out["dummy"] = cpu_baseline_of(lambda: oracle.dummy_packed(2048), T(2048), "cells/s",
+                                   "oracle.dummy_packed(n=2048): all 2,098,176 cells")
+    pts = inputs.points(EDM_N, 3, 42)
+    rows = 1024
+    out["edm"] = cpu_baseline_of(lambda: oracle.edm(pts, EDM_N - rows, EDM_N), T(EDM_N) - T(EDM_N - rows), "cells/s",
+                                 f"oracle.edm rows [{EDM_N - rows}, {EDM_N}) of n={EDM_N}")
+    pts4 = inputs.points(EDM_N, 4, 42)
+    out["edm_dim4"] = cpu_baseline_of(lambda: oracle.edm(pts4, EDM_N - rows, EDM_N), T(EDM_N) - T(EDM_N - rows),
+                                      "cells/s", f"oracle.edm (4 features) rows [{EDM_N - rows}, {EDM_N}) of n={EDM_N}")
+    sph = inputs.spheres(200000, 42)
+    r0, r1 = 200000 - 256, 200000
+    out["collide"] = cpu_baseline_of(lambda: oracle.collide(sph, r0, r1), T(r1 - 1) - T(r0 - 1), "pair tests/s",
+                                     f"oracle.collide rows [{r0}, {r1}) of n=200000 (all j < i)")
+    iv = inputs.intervals(200000, 42, 1e-5)
+    out["collide1d"] = cpu_baseline_of(lambda: oracle.collide1d(iv, r0, r1), T(r1 - 1) - T(r0 - 1), "pair tests/s",
+                                       f"oracle.collide1d rows [{r0}, {r1}) of n=200000")
+    n = 32768
+    st = inputs.ca_state(n, 42)
+    c0, c1 = n - 512, n
+    out["ca"] = cpu_baseline_of(lambda: oracle.ca_step_rows(n, st, c0, c1), T(c1) - T(c0), "cell-updates/s",
+                                f"oracle.ca_step_rows rows [{c0}, {c1}) of n={n}, one generation")
+    x = inputs.points4(4096, 42)[:384]
+    out["triplet"] = cpu_baseline_of(lambda: oracle.triplet_total(x), 384 * 383 * 382 // 6, "triplets/s",
+                                     "oracle.triplet_total on the first 384 of the n=4096 particles")
+    return out
+
+
 def cpu_edm_sample(target_s=10.0, max_rows=None):
     """Oracle EDM on a bounded band of rows at the bottom of the triangle (the
     longest rows), grown until one pass takes >= 1 s (or covers the whole
@@ -647,15 +849,24 @@ def main():
     if not args.only_edm:
         if world == 1:
             workloads["dummy"] = bench_dummy(pk)
+            workloads["edm_dim4"] = bench_edm4(pk)
         workloads["collide"] = bench_collide(rank, world, pk)
         workloads["collide1d"] = bench_collide1d(rank, world, pk)
-        workloads["ca"] = bench_ca(rank, world, pk)
+        workloads["ca"] = bench_ca(rank, world, pk, r["clocks"])
         workloads["triplet"] = bench_triplet(rank, world, pk)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, desc, cores, _ = cpu_edm_sample(target_s=10.0)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+               "cpu_model": cpu_model()}
+        if not args.only_edm:
+            for k, v in cpu_baselines().items():
+                if k == "edm":
+                    cpu["value_1core"] = v["value_1core"]
+                    cpu["sample_1core"] = v["sample"]
+                elif k in workloads:
+                    workloads[k]["cpu_baseline"] = v
 
     if rank == 0:
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -54,7 +54,8 @@ typedef enum {
 } tri_status;
 
 enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2, TRI_LAMBDA_CLC = 7 };
-/* tri_collide only, rho = 256, 384 or 512 (384: these strategies only): the filter gap
+/* tri_collide only, rho = 128 k for k = 2..8 (256 and 512 are also SIMT tile edges; the others
+ * belong to these strategies only): the filter gap
  * evaluated on the 5th-generation tensor cores (tcgen05.mma into TMEM,
  * csrc/collide_tc.cu); the count is the same exact fixed-order predicate (reading Q9).
  * TRI_LAMBDA_TC runs the TRI_LAMBDA grid (one CTA per tile omega), TRI_BB_TC the same
@@ -188,7 +189,8 @@ tri_status tri_edm_host(const tri_map_t *map, int32_t strategy, const float *h_p
  *   d2 = fma(dz,dz, fma(dy,dy, dx*dx)) < (ri + rj)^2
  * evaluated in IEEE fp32 round-to-nearest with exactly that operation order.
  * d_spheres: n x 4 floats (x, y, z, r), 16-byte aligned, spheres_bytes >= 16 n.
- * count_bytes >= 8.  rho in {128,256,512} (and 384 for TRI_LAMBDA_TC).
+ * count_bytes >= 8.  rho in {128,256,512} (SIMT strategies) or 128 k, k = 2..8 (tensor-core
+ * strategies).
  * The map must be built with diag = 1 (tiles) -- the strict filter is per pair.
  * TRI_LAMBDA_TC / TRI_BB_TC need d_ws (tri_collide_workspace_size bytes, 16-byte
  * aligned).  If a tensor-core or bulk-copy completion ever fails to arrive within ~2 s

@@ -66,6 +66,8 @@ def lib():
         L.orc_triplet_abs.argtypes = [i64, vp, ctypes.c_double, i64, i64, vp]
         L.orc_triplet_total.argtypes = [i64, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_threads.restype = None
         L.orc_variant_scan.argtypes = [i32, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]
         L.orc_collide1d.argtypes = [i64, vp, i64, i64, ctypes.POINTER(u64)]
         _lib = L
@@ -84,6 +86,11 @@ def _ptr(a: np.ndarray):
 
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_threads(k: int) -> None:
+    """OpenMP threads of later oracle calls (k < 1: all cores)."""
+    lib().orc_set_threads(int(k))
 
 
 # --- figurate numbers ----------------------------------------------------

@@ -514,3 +514,13 @@ int orc_num_threads(void)
     return 1;
 #endif
 }
+
+/* Thread count of later calls (bench.py's one-core oracle timing); k < 1: all cores. */
+void orc_set_threads(int k)
+{
+#ifdef _OPENMP
+    omp_set_num_threads(k >= 1 ? k : omp_get_num_procs());
+#else
+    (void)k;
+#endif
+}

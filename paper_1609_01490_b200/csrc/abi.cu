@@ -225,8 +225,9 @@ tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_sp
     g_launches = 0;
     const bool tc = strategy == TRI_LAMBDA_TC || strategy == TRI_BB_TC;
     if (bad_map(map) || (bad_strategy(strategy) && !tc) || !d_spheres || !d_count) return TRI_EINVAL;
-    if (map->rho != 128 && map->rho != 256 && map->rho != 384 && map->rho != 512) return TRI_EINVAL;
-    if (map->rho == 384 && !tc) return TRI_EINVAL;                            // tcgen05 tile edge only
+    if (tc ? (map->rho % 128 || map->rho < 256 || map->rho > 1024)     // tcgen05: 256, 384, ..., 1024
+           : (map->rho != 128 && map->rho != 256 && map->rho != 512))
+        return TRI_EINVAL;
     if (((uintptr_t)d_spheres & 15u) != 0 || (((uintptr_t)d_count) & 7u)) return TRI_EINVAL;
     if (spheres_bytes / 16u < (uint64_t)map->n || count_bytes < 8) return TRI_EINVAL;
     if (tc) {

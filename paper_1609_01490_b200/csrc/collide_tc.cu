@@ -13,8 +13,9 @@
 //   A_i  = |q_i|^2 - R_i^2 - kappa u M_i,  M_i = |q_i|^2 + R_i^2   (fp64), split into
 //          A_i = Ab_i + As_i + res_i with Ab, As TF32 and |res_i| <= 2^-21 M_i
 //   X_i  = ( qx,  qy,  qz,  R, Ab, As, 1, 1)            row operand (A, K-major)
-//   Y_j  = (-2qx,-2qy,-2qz,-2R, 1,  1, Ab, As)          column operand (B, K-major)
-//   g_ij = X_i . Y_j = |q_i - q_j|^2 - (R_i + R_j)^2 - kappa u (M_i + M_j) - res_i - res_j
+//   Y_j  = S (-2qx,-2qy,-2qz,-2R, 1,  1, Ab, As)        column operand (B, K-major), S = 2^20
+//   g_ij = X_i . Y_j = S (|q_i - q_j|^2 - (R_i + R_j)^2 - kappa u (M_i + M_j) - res_i - res_j)
+// (S is a power of two: exact, and it changes no sign.)
 // Why it is conservative: the fp32 predicate counts only if the real distance satisfies
 // d < (1 + 4.1u)(r_i + r_j) (three roundings in d2, two in s*s); then |q_i - q_j| <=
 // d + e_i + e_j < R_i + R_j, so the exact value of X_i . Y_j is < -kappa u (M_i + M_j) +
@@ -31,19 +32,26 @@
 // copies (cp.async.bulk, the TMA engine) completing on an mbarrier.
 //
 // CTA = 128 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB
-// grid); 128 TMEM columns (4 CTAs per SM hold all 512); per 128 x 128 block
-// one tcgen05.mma (issued by one thread), commit -> mbarrier, then the epilogue:
-// thread t = accumulator lane t = row t of the block, tcgen05.ld 32 columns at a time,
-// sign bits OR-ed by LOP3 (ALU pipe) and counted by IMAD.HI (FMA pipe) so both pipes
-// share the work.  A flagged 32-column group recounts only its negative columns, from
-// registers.  Diagonal tiles skip the blocks above the diagonal and recount j < i only.
+// grid), 128 TMEM columns, 3 CTAs per SM.  Per 128 x 128 block one
+// tcgen05.mma (issued by one thread) commits to an mbarrier; thread t = accumulator lane
+// t = row t of the block loads all 128 columns into registers (4 x tcgen05.ld.32x32b.x32),
+// the CTA hands the accumulator back (one barrier) and thread 0 issues the next block's
+// MMA while every thread tests its values: 21 of each 32 by 3-input LOP3 ORs of the sign
+// bits (ALU pipe), 11 by a saturating product P = sat(P g'), zero iff some g' <= 0 (FMA
+// pipe; the MMA computes g' = 2^20 g so every pair that is not within 1e-6 of touching has
+// g' >= 1 and leaves P = 1).  A flagged (row, 32-column group) recounts only its negative
+// columns, from registers.  Diagonal tiles skip the blocks above the diagonal and recount
+// j < i only.  Measured alternatives: persistent warp-specialised pipelines
+// (one MMA warp, or self-issuing warpgroups), an issuer warp per tile with one or two
+// accumulators, IMAD.HI sign counts -- all slower on B200.
 #include "tri_common.cuh"
 
 namespace {
 
-constexpr int kThreads = 128, kCols = 128;
+constexpr int kThreads = 128, kCols = 128, kCtasPerSm = 3;
 constexpr double kKappaU = 1.0 / 65536.0;               // 2^-16
 constexpr float kPad = 1.0e30f;                         // pad-row operand: g = 1e30 > 0
+constexpr float kScale = 1048576.0f;                    // S = 2^20: the column operand's scale
 
 struct TcArgs {
     const float4 *sph;
@@ -51,7 +59,6 @@ struct TcArgs {
     int64_t n, npad;
     uint64_t omega_begin, omega_end;
     unsigned long long *count;
-    uint32_t two;                 // = 2, a runtime value so ptxas keeps IMAD.HI (FMA pipe)
 };
 
 // The ABI's exact fixed-order predicate (reading Q9).
@@ -107,6 +114,8 @@ __global__ void collide_tc_prep(const float4 *__restrict__ sph, int64_t n, int64
         x[0] = qx; x[1] = qy; x[2] = qz; x[3] = R; x[4] = ab; x[5] = as; x[6] = 1.f; x[7] = 1.f;
         y[0] = -2.f * qx; y[1] = -2.f * qy; y[2] = -2.f * qz; y[3] = -2.f * R; y[4] = 1.f; y[5] = 1.f;
         y[6] = ab; y[7] = as;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y[k] *= kScale;
         if (A != A) {                                  // NaN: the predicate never counts it -> a pad row
 #pragma unroll
             for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
@@ -116,7 +125,7 @@ __global__ void collide_tc_prep(const float4 *__restrict__ sph, int64_t n, int64
 #pragma unroll
             for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
             x[4] = -kPad;
-            y[4] = 1.f;
+            y[4] = kScale;
             y[6] = -kPad;
         }
     } else {                                           // pad row / column: g = 1e30 against real ones
@@ -154,22 +163,23 @@ __device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db) {
         "l"(da), "l"(db), "r"(0), "r"(kIdesc));
 }
 
-// Wait for an mbarrier phase.  A completion that never arrives (a broken tensor-core or
-// copy path) must not hang the GPU or leave a plausible count: after ~2 s the count gets
-// its sticky invalid bit 63 (include/tri.h) and the kernel traps.
+// Wait for an mbarrier phase (the thread parks on the barrier until the phase completes or
+// the suspend-time hint expires).  A completion that never arrives (a broken tensor-core
+// or copy path) must not hang the GPU or leave a plausible count: after ~2 s the count
+// gets its sticky invalid bit 63 (include/tri.h) and the kernel traps.
 __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity, unsigned long long *count) {
     long long t0 = 0;
     for (int it = 0;; ++it) {
         uint32_t done;
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.b32 %0, 1, 0, p;\n\t}\n"
             : "=r"(done)
-            : "r"(mb), "r"(parity)
+            : "r"(mb), "r"(parity), "r"(0x989680)
             : "memory");
         if (done) return;
-        if (it == 64) t0 = clock64();
-        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > 4000000000ll) {
+        if (it == 8) t0 = clock64();
+        if (it > 8 && (it & 15) == 0 && clock64() - t0 > 4000000000ll) {
             if (count) atomicOr(count, 1ull << 63);
             __trap();
         }
@@ -188,22 +198,43 @@ __device__ __forceinline__ void ldtm32(uint32_t ta, uint32_t (&v)[32]) {
         : "r"(ta));
 }
 
-// Nonzero iff some value of the group has its sign bit set.  kFma of the 32 values are
-// tested on the FMA pipe (hi(2 v) = v >> 31 by IMAD.HI, summed), the rest by 3-input
-// LOP3 ORs on the ALU pipe.
-template <int kFma>
-__device__ __forceinline__ uint32_t any_negative(const uint32_t (&v)[32], uint32_t two) {
-    constexpr int kAlu = 32 - kFma;
-    static_assert(kAlu >= 3 && (kAlu - 3) % 2 == 0, "ALU share: 3 + 2k values");
+__device__ __forceinline__ uint32_t or3(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t o;
-    asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(v[0]), "r"(v[1]), "r"(v[2]));
-#pragma unroll
-    for (int e = 3; e < kAlu; e += 2) asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(o), "r"(v[e]), "r"(v[e + 1]));
-    uint32_t c = o >> 31;
-#pragma unroll
-    for (int e = kAlu; e < 32; ++e) asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(c) : "r"(v[e]), "r"(two), "r"(c));
-    return c;
+    asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(a), "r"(b), "r"(c));
+    return o;
 }
+
+__device__ __forceinline__ float mul_sat(float p, uint32_t g) {
+    float r;
+    asm("mul.rn.sat.f32 %0, %1, %2;" : "=f"(r) : "f"(p), "f"(__uint_as_float(g)));
+    return r;
+}
+
+// The sign test of one 32-column group.  Values [0, 32 - kFmul): OR of their bit patterns
+// by 3-input LOP3s (ALU pipe; bit 31 of `o` set iff one is negative).  Values
+// [32 - kFmul, 32): P = sat(... sat(sat(1 g'_a) g'_b) ...) by saturating FMULs (FMA pipe):
+// P stays in [0, 1] and is 0 iff some g' <= 0 (or P underflowed on values g' in (0, 1):
+// only a false flag).  The group is flagged iff o < 0 or P == 0.
+template <int kFmul>
+struct Signs {
+    uint32_t o;
+    float p;
+    __device__ __forceinline__ explicit Signs(const uint32_t (&v)[32]) {
+        constexpr int kAlu = 32 - kFmul;
+        static_assert(kAlu >= 3 && (kAlu - 3) % 2 == 0 && kFmul >= 1, "ALU share: 3 + 2k values");
+        o = or3(v[0], v[1], v[2]);
+#pragma unroll
+        for (int e = 3; e < kAlu; e += 2) o = or3(o, v[e], v[e + 1]);
+        float p0 = mul_sat(1.0f, v[kAlu]), p1 = 1.0f;
+#pragma unroll
+        for (int e = kAlu + 1; e < 32; ++e) {
+            if ((e - kAlu) & 1) p1 = mul_sat(p1, v[e]);
+            else p0 = mul_sat(p0, v[e]);
+        }
+        p = p0 * p1;
+    }
+    __device__ __forceinline__ bool flagged() const { return (int32_t)o < 0 || p == 0.0f; }
+};
 
 // bit e set iff value e of the group is negative (only for flagged groups: rare)
 __device__ __forceinline__ uint32_t neg_mask(const uint32_t (&v)[32]) {
@@ -229,8 +260,21 @@ __device__ __noinline__ uint32_t recount(const float4 *sph, int64_t n, uint32_t 
     return cnt;
 }
 
-template <int kRho, bool kBB, int kFma>
-__global__ void __launch_bounds__(kThreads, 4) collide_tc_kernel(TcArgs a) {
+template <int R>
+__device__ __forceinline__ void block_of(bool diag, int idx, int &rh, int &ch) {
+    if (diag) {                                        // triangular block index -> (rh, ch), ch <= rh
+        rh = 0;
+#pragma unroll
+        for (int r = 1; r < R; ++r) rh += idx >= r * (r + 1) / 2;
+        ch = idx - rh * (rh + 1) / 2;
+    } else {
+        rh = idx / R;
+        ch = idx - rh * R;
+    }
+}
+
+template <int kRho, bool kBB, int kFmul>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs a) {
     constexpr int R = kRho / 128;
     constexpr uint32_t kOpBytes = kRho * 32;
     extern __shared__ __align__(1024) unsigned char dsm[];
@@ -279,48 +323,49 @@ __global__ void __launch_bounds__(kThreads, 4) collide_tc_kernel(TcArgs a) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = taddr;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-    if (t == 0) mbar_wait(mb_ld, 0, a.count);
+    const uint32_t lanes = tmem + ((uint32_t)(warp * 32) << 16);
     const bool diag = bi == bj;
-    uint32_t cnt = 0, phase = 0;
+    const int nblk = diag ? R * (R + 1) / 2 : R * R;
+    auto issue = [&](int idx) {
+        int rh, ch;
+        block_of<R>(diag, idx, rh, ch);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        mma(tmem, smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_mma)
+                     : "memory");
+    };
+    if (t == 0) {
+        mbar_wait(mb_ld, 0, a.count);
+        issue(0);
+    }
+    uint32_t cnt = 0;
 #pragma unroll 1
-    for (int rh = 0; rh < R; ++rh) {
-        const int64_t i = (int64_t)bi * kRho + rh * 128 + t;        // this thread's row
-#pragma unroll 1
-        for (int ch = 0; ch < (diag ? rh + 1 : R); ++ch) {
-            if (t == 0) {
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                mma(tmem, smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
-                asm volatile(
-                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_mma)
-                    : "memory");
-            }
-            mbar_wait(mb_mma, phase, a.count);
-            phase ^= 1u;
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const int64_t j0 = (int64_t)bj * kRho + ch * 128;
-            // strict j < i inside a diagonal block: columns [0, t) of the block's 128
-            const int jlim = (diag && ch == rh) ? t : 128;
+    for (int idx = 0; idx < nblk; ++idx) {
+        mbar_wait(mb_mma, (uint32_t)idx & 1u, a.count);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint32_t v[4][32];
 #pragma unroll
-            for (int cg = 0; cg < kCols / 32; cg += 2) {
-                uint32_t v0[32], v1[32];
-                ldtm32(lane_base + (uint32_t)(cg * 32), v0);
-                ldtm32(lane_base + (uint32_t)(cg * 32 + 32), v1);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const uint32_t f0 = any_negative<kFma>(v0, a.two), f1 = any_negative<kFma>(v1, a.two);
-                if (f0 | f1) {
-                    if (f0) cnt += recount(a.sph, a.n, neg_mask(v0), i, j0 + cg * 32, jlim - cg * 32);
-                    if (f1) cnt += recount(a.sph, a.n, neg_mask(v1), i, j0 + cg * 32 + 32, jlim - cg * 32 - 32);
-                }
-            }
-            // every lane's loads are done before the next MMA overwrites the accumulator
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncthreads();
+        for (int cg = 0; cg < 4; ++cg) ldtm32(lanes + (uint32_t)(cg * 32), v[cg]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // the accumulator is in registers: hand it back, the next MMA runs during the tests
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (t == 0 && idx + 1 < nblk) issue(idx + 1);
+        const Signs<kFmul> s0(v[0]), s1(v[1]), s2(v[2]), s3(v[3]);
+        if ((int32_t)(or3(s0.o, s1.o, s2.o) | s3.o) < 0 || s0.p * s1.p * (s2.p * s3.p) == 0.0f) {   // rare
+            int rh, ch;
+            block_of<R>(diag, idx, rh, ch);
+            const int64_t i = (int64_t)bi * kRho + rh * 128 + t;
+            const int64_t j0 = (int64_t)bj * kRho + ch * 128;
+            const int jlim = (diag && ch == rh) ? t : 128;   // strict j < i inside a diagonal block
+            if (s0.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[0]), i, j0, jlim);
+            if (s1.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[1]), i, j0 + 32, jlim - 32);
+            if (s2.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[2]), i, j0 + 64, jlim - 64);
+            if (s3.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[3]), i, j0 + 96, jlim - 96);
         }
     }
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((t & 31) == 0 && cnt) atomicAdd(a.count, (unsigned long long)cnt);
 }
@@ -379,15 +424,19 @@ __global__ void __launch_bounds__(kThreads) tc_tf32_probe_kernel(const float *x,
 
 namespace tri {
 
-constexpr int kFmaShare = 9;          // values per 32 tested on the FMA pipe (A/B'd on B200)
+#ifndef TRI_TC_FMUL
+#define TRI_TC_FMUL 1
+#endif
+constexpr int kFmul = TRI_TC_FMUL;   // values of each 32 tested on the FMA pipe (A/B'd on B200)
 
 size_t collide_tc_ws_bytes(const tri_map_t &m) { return (size_t)m.m * (size_t)m.rho * 64u; }
 
 template <int kRho, bool kBB>
 static void launch_rho(const tri_map_t &m, TcArgs a, cudaStream_t st) {
-    // pad the dynamic smem so at most 4 CTAs share an SM: they hold all 512 TMEM columns
-    const int smem = 2 * kRho * 32 > 48 * 1024 ? 2 * kRho * 32 : 48 * 1024;
-    auto k = collide_tc_kernel<kRho, kBB, kFmaShare>;
+    // pad the dynamic smem so at most kCtasPerSm CTAs share an SM (their TMEM columns fit)
+    const int pad = 228 * 1024 / (kCtasPerSm + 1) + 1024;
+    const int smem = 2 * kRho * 32 > pad ? 2 * kRho * 32 : pad;
+    auto k = collide_tc_kernel<kRho, kBB, kFmul>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), kThreads, smem, st>>>(a);
     else k<<<tile_grid(a.omega_end - a.omega_begin), kThreads, smem, st>>>(a);
@@ -395,7 +444,7 @@ static void launch_rho(const tri_map_t &m, TcArgs a, cudaStream_t st) {
 
 tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph, unsigned long long *count,
                              void *ws, cudaStream_t st) {
-    if (m.rho != 256 && m.rho != 384 && m.rho != 512) return TRI_EINVAL;
+    if (m.rho % 128 || m.rho < 256 || m.rho > 1024) return TRI_EINVAL;
     if (strategy == TRI_BB_TC && m.m > 65535) return TRI_EINVAL;
     TcArgs a;
     a.sph = (const float4 *)sph;
@@ -405,12 +454,15 @@ tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph,
     a.omega_begin = m.omega_begin;
     a.omega_end = m.omega_end;
     a.count = count;
-    a.two = 2u;
     collide_tc_prep<<<(unsigned)((a.npad + 255) / 256), 256, 0, st>>>(a.sph, a.n, a.npad, (uint32_t *)ws, count);
     note_launches(1);
     if (a.omega_end > a.omega_begin) {
         const bool bb = strategy == TRI_BB_TC;
-        if (m.rho == 512) bb ? launch_rho<512, true>(m, a, st) : launch_rho<512, false>(m, a, st);
+        if (m.rho == 1024) bb ? launch_rho<1024, true>(m, a, st) : launch_rho<1024, false>(m, a, st);
+        else if (m.rho == 896) bb ? launch_rho<896, true>(m, a, st) : launch_rho<896, false>(m, a, st);
+        else if (m.rho == 768) bb ? launch_rho<768, true>(m, a, st) : launch_rho<768, false>(m, a, st);
+        else if (m.rho == 640) bb ? launch_rho<640, true>(m, a, st) : launch_rho<640, false>(m, a, st);
+        else if (m.rho == 512) bb ? launch_rho<512, true>(m, a, st) : launch_rho<512, false>(m, a, st);
         else if (m.rho == 384) bb ? launch_rho<384, true>(m, a, st) : launch_rho<384, false>(m, a, st);
         else bb ? launch_rho<256, true>(m, a, st) : launch_rho<256, false>(m, a, st);
         note_launches(1);

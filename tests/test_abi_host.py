@@ -145,11 +145,12 @@ def test_ca_steps_p2p_validation(L):
     assert L.tri_ipc_close(None) == tri.TRI_EINVAL
 
 
-def test_collide_rho384_is_tc_only(L):
-    """rho = 384 is a tile edge of the tcgen05 collision kernel only: the SIMT strategies
-    reject it with EINVAL before any launch (fake device pointers)."""
+@pytest.mark.parametrize("rho", [384, 640, 768, 1024])
+def test_collide_rho384_is_tc_only(L, rho):
+    """rho = 384, 640, ..., 1024 are tile edges of the tcgen05 collision kernel only: the
+    SIMT strategies reject them with EINVAL before any launch (fake device pointers)."""
     import ctypes
-    m = tri.tri_map_init(1000, 384)
+    m = tri.tri_map_init(1000, rho)
     for strat in (tri.TRI_LAMBDA, tri.TRI_BB, tri.TRI_LAMBDA_PERSIST):
         assert L.tri_collide(ctypes.byref(m), strat, ctypes.c_void_p(1 << 20), 16 * 1000,
                              ctypes.c_void_p(2 << 20), 8, None, 0, None) == tri.TRI_EINVAL

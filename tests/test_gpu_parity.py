@@ -318,7 +318,7 @@ def test_collide_knife_edge_pairs(orc, offset, scale):
 
 
 @pytest.mark.parametrize("strategy", ["tc", "bb_tc"])
-@pytest.mark.parametrize("rho", [256, 384, 512])
+@pytest.mark.parametrize("rho", [256, 384, 512, 640, 1024])
 @pytest.mark.parametrize("n,seed,rmax", [(1, 7, 0.1), (300, 42, 0.2), (1000, 42, 0.05), (5000, 7, 0.02),
                                          (777, 42, 0.08), (1153, 7, 0.3)])
 def test_collide_tc_small(orc, n, seed, rmax, rho, strategy):
@@ -333,7 +333,7 @@ def test_collide_tc_small(orc, n, seed, rmax, rho, strategy):
 
 
 @pytest.mark.parametrize("strategy", ["tc", "bb_tc"])
-@pytest.mark.parametrize("rho", [256, 384, 512])
+@pytest.mark.parametrize("rho", [256, 384, 512, 768, 1024])
 @pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (0.5, 1.0), (100.0, 1.0), (-1000.0, 10.0), (0.0, 1e-3),
                                           (0.49, 1e-4), (3.0, 0.1)])
 def test_collide_tc_knife_edge(orc, offset, scale, rho, strategy):
@@ -349,15 +349,15 @@ def test_collide_tc_full_size_rank_slice(orc):
     n = 200000
     s = inputs.spheres(n, 42)
     d = torch.from_numpy(s).cuda()
-    for g, rho in ((0, 256), (40, 256), (0, 512), (20, 512), (30, 384)):
-        m = tri.tri_map_init(n, rho, 1, g, {256: 256, 384: 170, 512: 128}[rho], 1)   # snapped: whole rows
+    for g, rho in ((0, 256), (40, 256), (0, 512), (20, 512), (30, 384), (0, 1024), (9, 1024)):
+        m = tri.tri_map_init(n, rho, 1, g, {256: 256, 384: 170, 512: 128, 1024: 64}[rho], 1)   # snapped rows
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         tri.tri_collide(m, "tc", d, cnt)
         sync()
         assert cnt.item() == orc.collide(s, m.row_begin, m.row_end)
 
 
-@pytest.mark.parametrize("rho", [256, 384, 512])
+@pytest.mark.parametrize("rho", [256, 384, 512, 1024])
 def test_collide_tc_plain_ranks(orc, rho):
     """tcgen05 filter on plain (unsnapped) omega ranges of 3 ranks: the partial counts sum
     to the oracle's total (11-bit-quantised spheres: every fp32 op exact)."""

@@ -85,7 +85,7 @@ def test_tc_tf32_accumulation_bound(case):
     assert np.all(err <= 2.0 ** -20 * ab), ratio
 
 
-@pytest.mark.parametrize("strategy,rho", [("tc", 384), ("bb_tc", 256), ("tc", 512)])
+@pytest.mark.parametrize("strategy,rho", [("tc", 384), ("bb_tc", 256), ("tc", 512), ("tc", 1024), ("bb_tc", 1024)])
 def test_collide_tc_special_values(orc, strategy, rho):
     """NaN, infinite and huge coordinates or radii never break exactness: the filter
     treats them as never- or always-flagged and the exact predicate decides."""
@@ -115,8 +115,9 @@ def test_collide_tc_dense_cluster(orc, strategy):
     s = np.zeros((n, 4), np.float32)
     s[:, :3] = 0.3 + rng.random((n, 3)) * 1e-3
     s[:, 3] = 0.01
-    m = tri.tri_map_init(n, 384)
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
-    torch.cuda.synchronize()
-    assert cnt.item() == orc.collide(s) == n * (n - 1) // 2
+    for rho in (384, 1024):
+        m = tri.tri_map_init(n, rho)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tri.tri_collide(m, strategy, torch.from_numpy(s).cuda(), cnt)
+        torch.cuda.synchronize()
+        assert cnt.item() == orc.collide(s) == n * (n - 1) // 2, rho

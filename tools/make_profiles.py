@@ -61,7 +61,8 @@ def main():
         d = s[0]
         summ[name] = {"kernel": d["kernel"], "round": tag,
                       "dram_bytes_per_launch": to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"]),
-                      "duration": d["gpu__time_duration.sum"], "source": os.path.basename(out)}
+                      "duration": d["gpu__time_duration.sum"], "source": os.path.basename(out),
+                      "inst_per_launch": float(d.get("smsp__inst_executed.sum", "0 inst").split()[0])}
         print(out)
     json.dump(summ, open(sp, "w"), indent=1)
 
