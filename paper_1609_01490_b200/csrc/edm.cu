@@ -22,7 +22,11 @@
 // was measured: 1.386 -> 1.296 ms per isolated launch, but 1.40 -> 1.46 ms per
 // step in the bench's 200-launch sustained loop; the same store pattern with no
 // arithmetic at all is slower still there (1.47 ms): the packed layout's write
-// stream, not instruction issue, sets the pace, so the scalar path stays.)
+// stream, not instruction issue, sets the pace, so the scalar path stays.  Round 2
+// measured the same for row points from shared memory instead of shuffles, and for 32-B
+// chunks at rho = 128 with two rows per warp store (1.40 -> 1.80 ms); 5 CTAs per SM
+// (<= 48 registers) and float4 point loads for 4 features take the paper's 4-D EDM
+// from 2.59 to 1.55 ms.)
 #include "tri_common.cuh"
 
 namespace {
@@ -34,6 +38,7 @@ struct EdmArgs {
     int64_t tile_row_begin;
     uint64_t out_offset, out_cells;
     float *out;
+    bool vec4;                    // 4 features with ld % 4 == 0 and 16-byte aligned points
 };
 
 constexpr int kEdmThreads = 256;
@@ -101,8 +106,10 @@ __device__ __forceinline__ void chunk_phase(int delta, const float (&p)[DIM], co
 }
 
 // Interior tile: rows [r0, r0+RHO) x cols [c0, c0+RHO), c0 + RHO < r0.
-// One warp per row segment: lane k owns chunk k (RHO = 32 CW).
-template <int RHO, int DIM>
+// One warp per row segment: lane k owns chunk k (RHO = 32 CW).  VEC4 (4 features, rows
+// 16-byte aligned -- the paper's x, y, z, w points): points are read as float4,
+// the row point by one broadcast load instead of four shuffles.
+template <int RHO, int DIM, bool VEC4 = false>
 __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, int64_t c0) {
     constexpr int CW = ChunkW<RHO>::CW, WN = 2 * CW - 1;
     static_assert(RHO == 32 * CW, "one chunk per lane per row");
@@ -115,11 +122,16 @@ __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, 
 #pragma unroll
     for (int t = 0; t < WN; ++t) {
         const int64_t col = c0 + CW * lane + t;               // < r0: always a valid point
+        if constexpr (VEC4) {                                  // 4 features, 16-B rows: one LDG.128
+            const float4 q = __ldg(reinterpret_cast<const float4 *>(a.pts + col * a.ld));
+            w[0][t] = q.x; w[1][t] = q.y; w[2][t] = q.z; w[3][t] = q.w;
+        } else {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) w[d][t] = __ldg(a.pts + col * a.ld + d);
+            for (int d = 0; d < DIM; ++d) w[d][t] = __ldg(a.pts + col * a.ld + d);
+        }
     }
     float pr[DIM];
-    {
+    if constexpr (!VEC4) {
         const int64_t rr = rbase + (lane < ROWS ? lane : 0);
         const bool in = rr < a.n;
 #pragma unroll
@@ -131,8 +143,13 @@ __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, 
 #pragma unroll 1
     for (int rr = 0; rr < nrows; ++rr) {
         float p[DIM];
+        if constexpr (VEC4) {                                  // the row point: one broadcast LDG.128
+            const float4 q = __ldg(reinterpret_cast<const float4 *>(a.pts + (rbase + rr) * a.ld));
+            p[0] = q.x; p[1] = q.y; p[2] = q.z; p[3 % DIM] = q.w;
+        } else {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) p[d] = __shfl_sync(0xffffffffu, pr[d], rr);
+            for (int d = 0; d < DIM; ++d) p[d] = __shfl_sync(0xffffffffu, pr[d], rr);
+        }
         const int delta = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1));
         chunk_phase<DIM, CW>(delta, p, w, base + (s + (uint64_t)delta));
         s += (uint64_t)(rbase + rr + 1);               // T(i+1) = T(i) + i + 1
@@ -179,14 +196,18 @@ __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, i
 template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-    if (RHO >= 128 && bj + 1 < bi)
-        edm_tile_interior<(RHO >= 128 ? RHO : 128), DIM>(a, r0, c0);
-    else
-        edm_tile_checked<RHO, DIM>(a, r0, c0);
+    if constexpr (RHO >= 128) {
+        if (bj + 1 < bi) {
+            if (DIM == 4 && a.vec4) edm_tile_interior<RHO, DIM, DIM == 4>(a, r0, c0);
+            else edm_tile_interior<RHO, DIM>(a, r0, c0);
+            return;
+        }
+    }
+    edm_tile_checked<RHO, DIM>(a, r0, c0);
 }
 
 template <int RHO, int DIM, int STRAT>
-__global__ void __launch_bounds__(kEdmThreads) edm_kernel(EdmArgs a) {
+__global__ void __launch_bounds__(kEdmThreads, 5) edm_kernel(EdmArgs a) {
     if (STRAT == TRI_BB) {
         const uint32_t bj = blockIdx.x;
         const uint32_t bi = blockIdx.y + (uint32_t)a.tile_row_begin;
@@ -275,6 +296,7 @@ tri_status launch_edm(const tri_map_t &m, int strategy, const float *pts, int di
     a.tile_row_begin = 0;
     a.out_offset = m.out_offset; a.out_cells = m.out_cells;
     a.out = out;
+    a.vec4 = dim == 4 && (ld & 3) == 0 && (((uintptr_t)pts) & 15u) == 0;
     switch (m.rho) {
         case 32: return launch_r<32>(m, strategy, dim, a, st);
         case 64: return launch_r<64>(m, strategy, dim, a, st);
