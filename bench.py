@@ -837,6 +837,9 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         if backend == "nccl":
+            # NCCL's init lines (rank count, NVLink / NVLS topology) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
@@ -879,6 +882,10 @@ def main():
                 "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
                 "clocks": r["clocks"], "vs_bb": r["vs_bb"],
                 "hbm_GBps": r["roofline"]["achieved"] * world, "workloads": workloads}
+        if world > 1:
+            line["dist"] = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                            "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                            if dist.get_backend() == "nccl" else None}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

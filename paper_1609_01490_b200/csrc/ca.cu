@@ -669,6 +669,9 @@ struct Multi {
         uint64_t seg[RHO];
     };
 
+// P2P: the slice's first / last k rows also go to the neighbours' halo buffers (peer
+// memory); a compile-time flag so the plain launch carries none of that logic.
+template <bool P2P>
 static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
     const int t = threadIdx.x;
     const int K = (int)a.k;
@@ -860,7 +863,7 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
     const int rr_hi = hi64 < 0 ? 0 : (hi64 > RHO ? RHO : (int)hi64);
     const int64_t dr64 = r0 - c0 + 1;                         // seg(rr) = dr + rr cells in the row from c0
     const int dr = dr64 > (1 << 20) ? (1 << 20) : (dr64 < -RHO ? -RHO : (int)dr64);
-    const bool p2p = a.peer_above != nullptr || a.peer_below != nullptr;
+    constexpr bool p2p = P2P;
     auto chunk = [](uint32_t h) {                             // 16 bits -> 16 bytes {0,1}
         return make_uint4(bits::spread4(h & 15u), bits::spread4((h >> 4) & 15u), bits::spread4((h >> 8) & 15u),
                           bits::spread4((h >> 12) & 15u));
@@ -925,6 +928,11 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
             }
         }
     }
+    // P2P: release the peer stores at system scope (NVLink): every store this thread made
+    // to a neighbour's halo buffer is performed before anything the thread -- hence the
+    // kernel, hence the stream's next operation (the epoch's all-reduce, whose completion
+    // the neighbour's next launch waits for) -- does afterwards.
+    if (P2P) __threadfence_system();
 }
 
 };
@@ -939,29 +947,29 @@ using G8 = Multi<224, 8, 2, 8>;     // rho = 224, k <= 8
 // per 8 generations (the first two steps measured before the store-phase rework).
 template <class M> constexpr int min_ctas() { return M::NW == 5 ? 7 : (M::NW == 6 ? 4 : 5); }
 
-template <class M, int STRAT>
+template <class M, int STRAT, bool P2P>
 __global__ void __launch_bounds__(M::NT, min_ctas<M>()) ca_multi_kernel(CaArgs a) {
     __shared__ __align__(16) typename M::Smem sm;
     if (STRAT == TRI_BB) {
         if (blockIdx.x > blockIdx.y + (uint32_t)a.tile_row_begin) return;
-        M::tile(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm);
+        M::template tile<P2P>(a, blockIdx.y + (uint32_t)a.tile_row_begin, blockIdx.x, sm);
     } else if (STRAT == TRI_LAMBDA) {
         const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
         if (w >= a.omega_end) return;
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
-        M::tile(a, bi, bj, sm);
+        M::template tile<P2P>(a, bi, bj, sm);
     } else {
 #pragma unroll 1
         for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
-            M::tile(a, t.bi, t.bj, sm);
+            M::template tile<P2P>(a, t.bi, t.bj, sm);
             __syncthreads();                                  // smem reused by the next tile
         }
     }
 }
 
-template <class M>
-tri_status launch_geom(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+template <class M, bool P2P>
+tri_status launch_geom_p(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
     constexpr int NT = M::NT;
     if (strategy == TRI_BB) {
         const int64_t tr0 = m.row_begin / m.rho;
@@ -969,22 +977,28 @@ tri_status launch_geom(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t 
         if (tr1 <= tr0) return TRI_OK;
         if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
         a.tile_row_begin = tr0;
-        ca_multi_kernel<M, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
+        ca_multi_kernel<M, TRI_BB, P2P><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), NT, 0, st>>>(a);
     } else if (strategy == TRI_LAMBDA) {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
-        ca_multi_kernel<M, TRI_LAMBDA><<<tri::tile_grid(nb), NT, 0, st>>>(a);
+        ca_multi_kernel<M, TRI_LAMBDA, P2P><<<tri::tile_grid(nb), NT, 0, st>>>(a);
     } else {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<M, TRI_LAMBDA_PERSIST>, NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_multi_kernel<M, TRI_LAMBDA_PERSIST, P2P>, NT, 0);
         uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
         if (g > nb) g = nb;
-        ca_multi_kernel<M, TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
+        ca_multi_kernel<M, TRI_LAMBDA_PERSIST, P2P><<<(unsigned)g, NT, 0, st>>>(a);
     }
     tri::note_launches(1);
     return tri::cuda_status();
+}
+
+template <class M>
+tri_status launch_geom(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
+    if (a.peer_above || a.peer_below) return launch_geom_p<M, true>(m, strategy, a, st);
+    return launch_geom_p<M, false>(m, strategy, a, st);
 }
 
 // rho = 128 (k <= 16) or rho = 224 (k <= 8); the caller has validated (rho, k).

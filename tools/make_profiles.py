@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import summarise  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("TRI_PROF_DIR", os.path.join(ROOT, "profiles"))
 
 
 def to_bytes(s):
