@@ -15,3 +15,15 @@ echo "== probe (tools/sanitizer_probe.py: tri_dummy told a 4 KB buffer holds 1 G
 echo "== sanitizer instruments libtri.so loaded through ctypes:" >> $OUT
 compute-sanitizer --tool memcheck --print-limit 2 python tools/sanitizer_probe.py 2>&1 | grep -E "Invalid|Device Frame" | head -2 >> $OUT
 cat $OUT
+# round 2: the tcgen05 collision kernel (TF32 operand prep, bulk copies, one MMA per block,
+# early accumulator hand-back) on both grids, every tile edge, special values
+echo "== compute-sanitizer on collide_tc_prep + collide_tc_kernel (TRI_LAMBDA_TC / TRI_BB_TC, rho 256..1024)" >> $OUT
+for tool in memcheck racecheck synccheck; do
+  if [ $tool = memcheck ]; then sel="collide_tc_small or collide_tc_knife_edge or collide_tc_special or collide_tc_dense or collide_tc_plain"
+  else sel="collide_tc_small and 1000-42"; fi
+  echo "== $tool: -k \"$sel\"" >> $OUT
+  compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
+    python -m pytest tests/test_gpu_parity.py tests/test_gpu_tc.py -q -x -p no:cacheprovider -k "$sel" 2>&1 | \
+    grep -E "passed|failed|ERROR SUMMARY|RACECHECK SUMMARY|Invalid|Hazard|error" | tail -6 >> $OUT
+done
+cat $OUT
