@@ -403,7 +403,7 @@ def bench_edm4(pk):
                          "frac": round(gbs / pk["hbm_gbs"], 4), "bytes_per_cell": 4}}
 
 
-COLLIDE_TC_RHO = 1024          # the tcgen05 kernel's best tile edge on B200 (256 ... 1024 measured)
+COLLIDE_TC_RHO = 768           # the tcgen05 kernel's best tile edge on B200 (256 ... 1024 measured; 768 = 4 CTAs per SM)
 
 
 def bench_collide(rank, world, pk):

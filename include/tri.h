@@ -56,8 +56,9 @@ typedef enum {
 enum { TRI_LAMBDA = 0, TRI_BB = 1, TRI_LAMBDA_PERSIST = 2, TRI_LAMBDA_CLC = 7 };
 /* tri_collide only, rho = 128 k for k = 2..8 (256 and 512 are also SIMT tile edges; the others
  * belong to these strategies only): the filter gap
- * evaluated on the 5th-generation tensor cores (tcgen05.mma into TMEM,
- * csrc/collide_tc.cu); the count is the same exact fixed-order predicate (reading Q9).
+ * evaluated on the 5th-generation tensor cores (one tcgen05.mma.kind::f16 per 128 x 128
+ * block into an F16 TMEM accumulator, csrc/collide_tc.cu); the count is the same exact
+ * fixed-order predicate (reading Q9).
  * TRI_LAMBDA_TC runs the TRI_LAMBDA grid (one CTA per tile omega), TRI_BB_TC the same
  * tile body on the m x m BB grid -- the like-for-like comparator. */
 enum { TRI_LAMBDA_TC = 8, TRI_BB_TC = 9 };
@@ -202,9 +203,10 @@ tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_sp
                        void *d_ws, size_t ws_bytes, void *stream);
 
 /* Device workspace tri_collide needs for `strategy` (bytes, 16-byte aligned; 0 for the
- * SIMT strategies, which accept d_ws = NULL).  TRI_LAMBDA_TC / TRI_BB_TC: m * rho * 64
- * bytes -- the TF32 row and column operands of every sphere (plus pad rows), written
- * by the call's first kernel and read by the tiles with bulk (TMA) copies. */
+ * SIMT strategies, which accept d_ws = NULL).  TRI_LAMBDA_TC / TRI_BB_TC: 256 + m * rho * 64
+ * bytes -- a header (the coordinate bound that picks the power-of-two scale) and the
+ * fp16 row and column operands of every sphere (plus pad rows), written by the call's
+ * first kernels and read by the tiles with bulk (TMA) copies. */
 size_t tri_collide_workspace_size(const tri_map_t *map, int32_t strategy);
 
 /* Test hook: D = X Y^T (128 x 128, fp32, row-major) from ONE tcgen05.mma.kind::tf32
@@ -212,6 +214,13 @@ size_t tri_collide_workspace_size(const tri_map_t *map, int32_t strategy);
  * low 13 mantissa bits are ignored).  It exposes the tensor core's fp32 accumulation
  * error, which the TRI_LAMBDA_TC filter's margin assumes bounded by 2^-20 sum |x y|. */
 tri_status tri_tc_tf32_probe(const float *d_x, const float *d_y, float *d_d, void *stream);
+
+/* Test hook: D (128 x 128 fp16 bit patterns, row-major) = X Y^T from ONE
+ * tcgen05.mma.kind::f16 128 x 128 x 16 with the caller's fp16 operands (row-major
+ * 128 x 16) into an F16 accumulator, read back with the packed 16-bit TMEM loads the
+ * collision filter uses.  The filter assumes the accumulator holds the correctly rounded
+ * value of a wide (>= fp32) sum of the products. */
+tri_status tri_tc_f16_probe(const void *d_x, const void *d_y, void *d_d, void *stream);
 
 /* 1-D collision count (reading Q10): *d_count (u64, zeroed by
  * the call) = number of pairs j < i with |c_i - c_j| < r_i + r_j, evaluated in IEEE

@@ -219,6 +219,12 @@ tri_status tri_tc_tf32_probe(const float *d_x, const float *d_y, float *d_d, voi
     return launch_tc_tf32_probe(d_x, d_y, d_d, (cudaStream_t)stream);
 }
 
+tri_status tri_tc_f16_probe(const void *d_x, const void *d_y, void *d_d, void *stream) {
+    g_launches = 0;
+    if (!d_x || !d_y || !d_d) return TRI_EINVAL;
+    return launch_tc_f16_probe(d_x, d_y, d_d, (cudaStream_t)stream);
+}
+
 tri_status tri_collide(const tri_map_t *map, int32_t strategy, const float *d_spheres, size_t spheres_bytes,
                        unsigned long long *d_count, size_t count_bytes, void *d_ws, size_t ws_bytes,
                        void *stream) {

@@ -1,4 +1,4 @@
-// collide_tc.cu -- TRI_LAMBDA_TC / TRI_BB_TC for tri_collide (rho = 256, 384 or 512): the
+// collide_tc.cu -- TRI_LAMBDA_TC / TRI_BB_TC for tri_collide (rho = 128 k, k = 2..8): the
 // collision filter of reading Q9 evaluated on the 5th-generation tensor cores.
 //
 // The count is the fixed-order fp32 predicate d2 < s*s over j < i (reading
@@ -6,56 +6,68 @@
 // filter value, and every (row, 32-column group) with a negative value is re-examined
 // with the exact predicate, so the count is exact.
 //
-// Filter (one kind::tf32 MMA per 128 x 128 block, K = 8, every operand exact in TF32):
-//   q_i  = tf32(p_i - c), c = (1/2, 1/2, 1/2)           quantised, centred position
-//   e_i  = |p_i - (q_i + c)|                            its exact Euclidean error (fp64)
-//   R_i  = tf32_up(r_i (1 + 8u) + e_i)                  inflated radius, u = 2^-24
-//   A_i  = |q_i|^2 - R_i^2 - kappa u M_i,  M_i = |q_i|^2 + R_i^2   (fp64), split into
-//          A_i = Ab_i + As_i + res_i with Ab, As TF32 and |res_i| <= 2^-21 M_i
-//   X_i  = ( qx,  qy,  qz,  R, Ab, As, 1, 1)            row operand (A, K-major)
-//   Y_j  = S (-2qx,-2qy,-2qz,-2R, 1,  1, Ab, As)        column operand (B, K-major), S = 2^20
-//   g_ij = X_i . Y_j = S (|q_i - q_j|^2 - (R_i + R_j)^2 - kappa u (M_i + M_j) - res_i - res_j)
-// (S is a power of two: exact, and it changes no sign.)
-// Why it is conservative: the fp32 predicate counts only if the real distance satisfies
-// d < (1 + 4.1u)(r_i + r_j) (three roundings in d2, two in s*s); then |q_i - q_j| <=
-// d + e_i + e_j < R_i + R_j, so the exact value of X_i . Y_j is < -kappa u (M_i + M_j) +
-// 2^-21 (M_i + M_j).  Products of TF32 values are exact in fp32; the tensor core's fp32
-// sum of the 8 products is within 2^-20 sum_k |X_ik Y_jk| <= 2^-20 * 2.01 (M_i + M_j) of
-// the exact sum (the accumulation bound, measured on B200 by tri_tc_tf32_probe and
-// tests/test_gpu_parity.py::test_tc_tf32_accumulation_bound on adversarial cancelling
-// operands).  With kappa u = 2^-16 the computed g_ij is therefore < 0.
+// Filter: one tcgen05.mma.kind::f16 per 128 x 128 block (fp16 operands, K = 16, of which
+// 8 are used) into an F16 accumulator.  Every operand is an exact fp16 value:
+//   2^-s        a power of two with |p - c| <= 1/2 and r <= 1/2 for every sphere after
+//               scaling (collide_tc_bounds; c = (1/2, 1/2, 1/2); s = 0 on the unit cube)
+//   q_i  = fp16((p_i - c) 2^-s)                       quantised, centred position
+//   e_i  = |(p_i - c) 2^-s - q_i|                      its Euclidean error (fp64, + slack)
+//   R_i  = fp16_up(r_i 2^-s (1 + 8u) + e_i)            inflated radius, u = 2^-24
+//   A_i  = |q_i|^2 - R_i^2 - kappa_u M_i - kappa_a,    M_i = |q_i|^2 + R_i^2 (fp64),
+//          = A1 + 2^-11 A2 + res, A1, A2 fp16, |res| <= 2^-24 |A| + 2^-36
+//   X_i  = ( q,    R,    A1,  A2,      1,     2^-11, 0 ... 0)      (A operand, K-major)
+//   Y_j  = S (-2q, -2R,  1,   2^-11,   A1_j,  A2_j,  0 ... 0)      (B operand), S = 2^15
+//   g_ij = X_i . Y_j = S (|q_i - q_j|^2 - (R_i + R_j)^2 - kappa (..)_i - kappa (..)_j - res)
+// Why it is conservative: the fp32 predicate counts only if the real distance d <
+// (1 + 4.1u)(r_i + r_j) (three roundings in d2, two in s*s); then |q_i - q_j| <= d 2^-s +
+// e_i + e_j < R_i + R_j, so the exact X_i . Y_j < -S (kappa_u (M_i + M_j) + 2 kappa_a -
+// |res_i| - |res_j|) < -S kappa_u (M_i + M_j) / 2 - S kappa_a.  fp16 x fp16 products are
+// exact; the tensor core sums them in (at least) fp32 precision -- within 2^-20 sum |terms|
+// <= 2^-20 2.01 S (M_i + M_j) of the exact sum -- and rounds ONCE to the F16 accumulator
+// (round to nearest, overflow to +-inf): both properties measured on B200
+// (tests/test_gpu_tc.py::test_tc_tf32_accumulation_bound, test_tc_f16_accumulator_rounding,
+// tools/probes/f16acc.cu).  With kappa_u = 2^-16 and kappa_a = 2^-24 the wide sum is below
+// -S kappa_a = -2^-9, a normal fp16 value, so the F16 result keeps its sign bit.
+// Pad rows past n and NaN spheres get operands that make every value positive; a sphere
+// outside the scaled range (|q| > 1/2, R > 1/2: only non-finite or extreme inputs) is
+// flagged against every row and column and decided by the exact predicate.
 //
-// Layout: tri_collide's caller-owned workspace holds X and Y for m * rho rows (pad rows
-// past n make every g positive) as canonical K-major no-swizzle core matrices: 8-row
-// group g at byte 256 g, K half h at +128 h, row r at +16 r -- so a tile's operands are
-// ONE contiguous rho x 32-byte run each, staged into shared memory by two 1-D bulk
-// copies (cp.async.bulk, the TMA engine) completing on an mbarrier.
+// Layout: tri_collide's caller-owned workspace = a 256-byte header (the bound) + X and Y
+// for m * rho rows as canonical K-major no-swizzle core matrices (8-row group g at byte
+// 256 g, K half h at +128 h, row r at +16 r: 32 bytes per row), so a tile's operands are
+// ONE contiguous rho x 32-byte run each, staged into shared memory by two 1-D bulk copies
+// (cp.async.bulk, the TMA engine) completing on an mbarrier.
 //
-// CTA = 128 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB
-// grid), 128 TMEM columns, 3 CTAs per SM.  Per 128 x 128 block one
-// tcgen05.mma (issued by one thread) commits to an mbarrier; thread t = accumulator lane
-// t = row t of the block loads all 128 columns into registers (4 x tcgen05.ld.32x32b.x32),
-// the CTA hands the accumulator back (one barrier) and thread 0 issues the next block's
-// MMA while every thread tests its values: 21 of each 32 by 3-input LOP3 ORs of the sign
-// bits (ALU pipe), 11 by a saturating product P = sat(P g'), zero iff some g' <= 0 (FMA
-// pipe; the MMA computes g' = 2^20 g so every pair that is not within 1e-6 of touching has
-// g' >= 1 and leaves P = 1).  A flagged (row, 32-column group) recounts only its negative
-// columns, from registers.  Diagonal tiles skip the blocks above the diagonal and recount
-// j < i only.  Measured alternatives: persistent warp-specialised pipelines
-// (one MMA warp, or self-issuing warpgroups), an issuer warp per tile with one or two
-// accumulators, IMAD.HI sign counts -- all slower on B200.
+// CTA = 128 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB grid,
+// P:411-418), 128 TMEM columns.  Per 128 x 128 block one MMA (issued by one thread)
+// commits to an mbarrier; thread t = accumulator lane t = row t of the block loads its 128
+// columns (4 x tcgen05.ld.32x32b.x16.pack::16b: two F16 values per register, 64
+// registers), the CTA hands the accumulator back (one barrier) and thread 0 issues the
+// next block's MMA while every thread ORs its 64 registers (32 three-input LOP3s: a
+// quarter of an ALU op per pair) and tests bits 15 and 31.  A flagged (row, 32-column)
+// group recounts only its negative columns with the exact predicate.  Diagonal tiles skip
+// the blocks above the diagonal and recount j < i only.  (Round 2 history in DESIGN.md:
+// the single-pass TF32 filter with F32 accumulators this replaces, persistent
+// warp-specialised pipelines, issuer warps -- all measured slower.)
+#include <cuda_fp16.h>
 #include "tri_common.cuh"
 
 namespace {
 
-constexpr int kThreads = 128, kCols = 128, kCtasPerSm = 3;
-constexpr double kKappaU = 1.0 / 65536.0;               // 2^-16
-constexpr float kPad = 1.0e30f;                         // pad-row operand: g = 1e30 > 0
-constexpr float kScale = 1048576.0f;                    // S = 2^20: the column operand's scale
+constexpr int kThreads = 128, kCols = 128;
+#ifndef TRI_TC_CTAS
+#define TRI_TC_CTAS 4
+#endif
+constexpr int kCtasPerSm = TRI_TC_CTAS;
+constexpr double kKappaU = 1.0 / 65536.0;               // 2^-16 (relative margin)
+constexpr double kKappaA = 1.0 / 16777216.0;            // 2^-24 (absolute margin, scaled units)
+constexpr float kS = 32768.0f;                          // S = 2^15: the column operand's scale
+constexpr float kPad = 60000.0f;                        // pad / extreme operand (fp16 range)
+constexpr int kHdrBytes = 256;                          // workspace header: the bound
 
 struct TcArgs {
     const float4 *sph;
-    const uint32_t *ops;          // workspace: X rows [0, npad), then Y rows [0, npad)
+    const uint16_t *ops;          // X rows [0, npad), then Y rows [0, npad): 16 halves each
     int64_t n, npad;
     uint64_t omega_begin, omega_end;
     unsigned long long *count;
@@ -69,76 +81,92 @@ __device__ __forceinline__ uint32_t hit(const float4 p, const float4 q) {
     return d2 < __fmul_rn(s, s) ? 1u : 0u;
 }
 
-__device__ __forceinline__ float tf32_rn(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
-// smallest TF32 value >= x (x >= 0, finite)
-__device__ __forceinline__ float tf32_up(float x) {
-    uint32_t b = __float_as_uint(x);
-    if (b & 0x1fffu) b = (b | 0x1fffu) + 1u;
-    return __uint_as_float(b);
-}
-
-// canonical K-major core-matrix slot of element k of row r
-__device__ __forceinline__ int slot(int64_t r, int k) {
-    return (int)(((r >> 3) * 64) + ((k >> 2) * 32) + ((r & 7) * 4) + (k & 3));
+// canonical K-major core-matrix slot (in halves) of element k (0..15) of row r
+__device__ __forceinline__ int64_t slot16(int64_t r, int k) {
+    return ((r >> 3) * 128) + ((k >> 3) * 64) + ((r & 7) * 8) + (k & 7);
 }
 
 // ---------------------------------------------------------------- operand preparation
-// One thread per row of [0, npad): the quantities of the header, in fp64 where an error
-// bound is computed, written as TF32 bit patterns.  Thread 0 also zeroes the count.
-__global__ void collide_tc_prep(const float4 *__restrict__ sph, int64_t n, int64_t npad, uint32_t *__restrict__ ops,
-                                unsigned long long *count) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *count = 0ull;
-    if (i >= npad) return;
-    float x[8], y[8];
-    if (i < n) {
+// hdr[0] = max over spheres of max(|x - 1/2|, |y - 1/2|, |z - 1/2|, |r|) as float bits
+// (non-negative floats order like their bit patterns; NaN is skipped).  Thread 0 also
+// zeroes the count.  hdr[0] is zeroed by the launcher before this kernel.
+__global__ void collide_tc_bounds(const float4 *__restrict__ sph, int64_t n, uint32_t *hdr,
+                                  unsigned long long *count) {
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 == 0) *count = 0ull;
+    float b = 0.f;
+    for (int64_t i = i0; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 p = __ldg(sph + i);
-        const float qx = tf32_rn(__fsub_rn(p.x, 0.5f)), qy = tf32_rn(__fsub_rn(p.y, 0.5f)),
-                    qz = tf32_rn(__fsub_rn(p.z, 0.5f));
-        // exact error of the quantised position: p, q and 1/2 are fp32, so every
-        // difference and sum below is exact in fp64 (up to the final sqrt / square)
-        const double ex = (double)p.x - ((double)qx + 0.5), ey = (double)p.y - ((double)qy + 0.5),
-                     ez = (double)p.z - ((double)qz + 0.5);
-        const double e = sqrt(ex * ex + ey * ey + ez * ez) * (1.0 + 0x1p-40) + 0x1p-60;
-        const double r = fabs((double)p.w) * (1.0 + 0x1p-21) + e;     // (1 + 8u) r + e, rounded up below
-        const float R = tf32_up(__double2float_ru(r));
-        const double q2 = (double)qx * qx + (double)qy * qy + (double)qz * qz, R2 = (double)R * R;
-        const double A = q2 - R2 - kKappaU * (q2 + R2);
-        const float ab = tf32_rn((float)A);
-        const float as = tf32_rn((float)(A - (double)ab));
-        x[0] = qx; x[1] = qy; x[2] = qz; x[3] = R; x[4] = ab; x[5] = as; x[6] = 1.f; x[7] = 1.f;
-        y[0] = -2.f * qx; y[1] = -2.f * qy; y[2] = -2.f * qz; y[3] = -2.f * R; y[4] = 1.f; y[5] = 1.f;
-        y[6] = ab; y[7] = as;
+        b = fmaxf(b, fmaxf(fmaxf(fabsf(p.x - 0.5f), fabsf(p.y - 0.5f)), fmaxf(fabsf(p.z - 0.5f), fabsf(p.w))));
+    }
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 16));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 8));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 4));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 2));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 1));
+    if ((threadIdx.x & 31) == 0 && b > 0.f) atomicMax(hdr, __float_as_uint(b));
+}
+
+// One thread per row of [0, npad): the quantities of the header, in fp64 where an error
+// bound is computed, written as fp16 bit patterns.
+__global__ void collide_tc_prep(const float4 *__restrict__ sph, int64_t n, int64_t npad, const uint32_t *hdr,
+                                uint16_t *__restrict__ ops) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npad) return;
+    // the scale 2^-s: |p - c| 2^-s <= 1/2 and r 2^-s <= 1/2 (bound = m 2^e, m in [1/2, 1))
+    const float bound = __uint_as_float(*hdr);
+    int s = 0;
+    if (bound > 0.5f && bound < 1e30f) {
+        int e;
+        frexpf(bound, &e);
+        s = e + 1;
+    }
+    const double sc = ldexp(1.0, -s);
+    float x[16], y[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) y[k] *= kScale;
-        if (A != A) {                                  // NaN: the predicate never counts it -> a pad row
-#pragma unroll
-            for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
-            x[4] = kPad;
-            y[6] = kPad;
-        } else if (!(fabs(A) < 1e30)) {                // huge: flagged against every real row / column
-#pragma unroll
-            for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
-            x[4] = -kPad;
-            y[4] = kScale;
-            y[6] = -kPad;
+    for (int k = 0; k < 16; ++k) { x[k] = 0.f; y[k] = 0.f; }
+    bool pad = i >= n, extreme = false;
+    if (!pad) {
+        const float4 p = __ldg(sph + i);
+        const double px = ((double)p.x - 0.5) * sc, py = ((double)p.y - 0.5) * sc, pz = ((double)p.z - 0.5) * sc;
+        const __half qx = __double2half(px), qy = __double2half(py), qz = __double2half(pz);
+        const double fx = __half2float(qx), fy = __half2float(qy), fz = __half2float(qz);
+        const double ex = px - fx, ey = py - fy, ez = pz - fz;
+        // + slack for the (p - 1/2) sc rounding in fp64 (relative 2^-53) and the sqrt
+        const double e = sqrt(ex * ex + ey * ey + ez * ez) * (1.0 + 0x1p-40) +
+                         (fabs(px) + fabs(py) + fabs(pz)) * 0x1p-50 + 0x1p-60;
+        const double rr = fabs((double)p.w) * sc * (1.0 + 0x1p-21) + e;
+        const __half R = __float2half_ru(__double2float_ru(rr));
+        const double fR = __half2float(R);
+        const double q2 = fx * fx + fy * fy + fz * fz, R2 = fR * fR;
+        const double A = q2 - R2 - kKappaU * (q2 + R2) - kKappaA;
+        if (p.x != p.x || p.y != p.y || p.z != p.z || p.w != p.w) {
+            pad = true;                                   // NaN: the predicate never counts it
+        } else if (!(fabs(fx) <= 0.5 && fabs(fy) <= 0.5 && fabs(fz) <= 0.5 && fR <= 0.5)) {
+            extreme = true;
+        } else {
+            const __half a1 = __double2half(A);
+            const __half a2 = __double2half((A - (double)__half2float(a1)) * 2048.0);
+            const float A1 = __half2float(a1), A2 = __half2float(a2);
+            x[0] = (float)fx; x[1] = (float)fy; x[2] = (float)fz; x[3] = (float)fR;
+            x[4] = A1; x[5] = A2; x[6] = 1.f; x[7] = 1.f / 2048.f;
+            y[0] = -2.f * kS * (float)fx; y[1] = -2.f * kS * (float)fy; y[2] = -2.f * kS * (float)fz;
+            y[3] = -2.f * kS * (float)fR; y[4] = kS; y[5] = kS / 2048.f; y[6] = kS * A1; y[7] = kS * A2;
         }
-    } else {                                           // pad row / column: g = 1e30 against real ones
-#pragma unroll
-        for (int k = 0; k < 8; ++k) { x[k] = 0.f; y[k] = 0.f; }
+    }
+    if (pad) {                                            // g = +60000 S against real rows / columns
         x[4] = kPad;
         y[6] = kPad;
+    } else if (extreme) {                                 // g < 0 against every real row / column
+        x[4] = -kPad;
+        y[4] = 1.f;
+        y[6] = -kPad;
     }
-    uint32_t *X = ops, *Y = ops + npad * 8;
+    uint16_t *X = ops, *Y = ops + npad * 16;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        X[slot(i, k)] = __float_as_uint(x[k]);
-        Y[slot(i, k)] = __float_as_uint(y[k]);
+    for (int k = 0; k < 16; ++k) {
+        X[slot16(i, k)] = __half_as_ushort(__float2half_rn(x[k]));   // every value is an exact fp16
+        Y[slot16(i, k)] = __half_as_ushort(__float2half_rn(y[k]));
     }
 }
 
@@ -152,15 +180,24 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     return d;                                         // base offset 0, lbo mode 0, SWIZZLE_NONE
 }
 
-// kind::tf32, fp32 accumulator, K-major A and B, M = 128, N = kCols
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCols >> 3) << 17) |
-                            ((uint32_t)(128 >> 4) << 24);
+// kind::f16: F16 accumulator (D format 0), F16 A and B (formats 0), K-major, M = 128, N = kCols
+constexpr uint32_t kIdescF16 = ((uint32_t)(kCols >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// kind::tf32, F32 accumulator (the accumulation probe)
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCols >> 3) << 17) |
+                                ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(0), "r"(kIdescF16));
+}
 
 __device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t}\n" ::"r"(tmem),
-        "l"(da), "l"(db), "r"(0), "r"(kIdesc));
+        "l"(da), "l"(db), "r"(0), "r"(kIdescTf32));
 }
 
 // Wait for an mbarrier phase (the thread parks on the barrier until the phase completes or
@@ -198,49 +235,35 @@ __device__ __forceinline__ void ldtm32(uint32_t ta, uint32_t (&v)[32]) {
         : "r"(ta));
 }
 
+// 32 F16 accumulator columns into 16 registers: column 2c in the low half of v[c], 2c + 1 in the high
+__device__ __forceinline__ void ldtm16p(uint32_t ta, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(ta));
+}
+
 __device__ __forceinline__ uint32_t or3(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t o;
     asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(o) : "r"(a), "r"(b), "r"(c));
     return o;
 }
 
-__device__ __forceinline__ float mul_sat(float p, uint32_t g) {
-    float r;
-    asm("mul.rn.sat.f32 %0, %1, %2;" : "=f"(r) : "f"(p), "f"(__uint_as_float(g)));
-    return r;
+// OR of 16 packed registers (32 F16 values): bit 15 / 31 set iff some even / odd column is negative
+__device__ __forceinline__ uint32_t or16(const uint32_t (&v)[16]) {
+    uint32_t o = or3(v[0], v[1], v[2]);
+#pragma unroll
+    for (int e = 3; e < 15; e += 2) o = or3(o, v[e], v[e + 1]);
+    return o | v[15];
 }
 
-// The sign test of one 32-column group.  Values [0, 32 - kFmul): OR of their bit patterns
-// by 3-input LOP3s (ALU pipe; bit 31 of `o` set iff one is negative).  Values
-// [32 - kFmul, 32): P = sat(... sat(sat(1 g'_a) g'_b) ...) by saturating FMULs (FMA pipe):
-// P stays in [0, 1] and is 0 iff some g' <= 0 (or P underflowed on values g' in (0, 1):
-// only a false flag).  The group is flagged iff o < 0 or P == 0.
-template <int kFmul>
-struct Signs {
-    uint32_t o;
-    float p;
-    __device__ __forceinline__ explicit Signs(const uint32_t (&v)[32]) {
-        constexpr int kAlu = 32 - kFmul;
-        static_assert(kAlu >= 3 && (kAlu - 3) % 2 == 0 && kFmul >= 1, "ALU share: 3 + 2k values");
-        o = or3(v[0], v[1], v[2]);
-#pragma unroll
-        for (int e = 3; e < kAlu; e += 2) o = or3(o, v[e], v[e + 1]);
-        float p0 = mul_sat(1.0f, v[kAlu]), p1 = 1.0f;
-#pragma unroll
-        for (int e = kAlu + 1; e < 32; ++e) {
-            if ((e - kAlu) & 1) p1 = mul_sat(p1, v[e]);
-            else p0 = mul_sat(p0, v[e]);
-        }
-        p = p0 * p1;
-    }
-    __device__ __forceinline__ bool flagged() const { return (int32_t)o < 0 || p == 0.0f; }
-};
-
-// bit e set iff value e of the group is negative (only for flagged groups: rare)
-__device__ __forceinline__ uint32_t neg_mask(const uint32_t (&v)[32]) {
+// bit e set iff column e of the 32-column group is negative (only for flagged groups: rare)
+__device__ __forceinline__ uint32_t neg_mask16(const uint32_t (&v)[16]) {
     uint32_t msk = 0;
 #pragma unroll
-    for (int e = 0; e < 32; ++e) msk |= (v[e] >> 31) << e;
+    for (int c = 0; c < 16; ++c) msk |= (((v[c] >> 15) & 1u) << (2 * c)) | ((v[c] >> 31) << (2 * c + 1));
     return msk;
 }
 
@@ -273,7 +296,7 @@ __device__ __forceinline__ void block_of(bool diag, int idx, int &rh, int &ch) {
     }
 }
 
-template <int kRho, bool kBB, int kFmul>
+template <int kRho, bool kBB>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs a) {
     constexpr int R = kRho / 128;
     constexpr uint32_t kOpBytes = kRho * 32;
@@ -301,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_mma));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // the tile's operand rows: two contiguous runs of the workspace -> shared memory
-        const uint32_t *gx = a.ops + (int64_t)bi * kRho * 8, *gy = a.ops + (a.npad + (int64_t)bj * kRho) * 8;
+        const uint16_t *gx = a.ops + (int64_t)bi * kRho * 16, *gy = a.ops + (a.npad + (int64_t)bj * kRho) * 16;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb_ld), "r"(2 * kOpBytes)
                      : "memory");
         asm volatile(
@@ -330,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs
         int rh, ch;
         block_of<R>(diag, idx, rh, ch);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        mma(tmem, smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
+        mma_f16(tmem, smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_mma)
                      : "memory");
     };
@@ -343,31 +366,36 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs
     for (int idx = 0; idx < nblk; ++idx) {
         mbar_wait(mb_mma, (uint32_t)idx & 1u, a.count);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        uint32_t v[4][32];
+        uint32_t v[4][16];
 #pragma unroll
-        for (int cg = 0; cg < 4; ++cg) ldtm32(lanes + (uint32_t)(cg * 32), v[cg]);
+        for (int cg = 0; cg < 4; ++cg) ldtm16p(lanes + (uint32_t)(cg * 32), v[cg]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         // the accumulator is in registers: hand it back, the next MMA runs during the tests
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
         if (t == 0 && idx + 1 < nblk) issue(idx + 1);
-        const Signs<kFmul> s0(v[0]), s1(v[1]), s2(v[2]), s3(v[3]);
-        if ((int32_t)(or3(s0.o, s1.o, s2.o) | s3.o) < 0 || s0.p * s1.p * (s2.p * s3.p) == 0.0f) {   // rare
+        const uint32_t o0 = or16(v[0]), o1 = or16(v[1]), o2 = or16(v[2]), o3 = or16(v[3]);
+        if ((or3(o0, o1, o2) | o3) & 0x80008000u) {          // rare: some value of the row is negative
             int rh, ch;
             block_of<R>(diag, idx, rh, ch);
             const int64_t i = (int64_t)bi * kRho + rh * 128 + t;
             const int64_t j0 = (int64_t)bj * kRho + ch * 128;
             const int jlim = (diag && ch == rh) ? t : 128;   // strict j < i inside a diagonal block
-            if (s0.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[0]), i, j0, jlim);
-            if (s1.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[1]), i, j0 + 32, jlim - 32);
-            if (s2.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[2]), i, j0 + 64, jlim - 64);
-            if (s3.flagged()) cnt += recount(a.sph, a.n, neg_mask(v[3]), i, j0 + 96, jlim - 96);
+            if (o0 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[0]), i, j0, jlim);
+            if (o1 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[1]), i, j0 + 32, jlim - 32);
+            if (o2 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[2]), i, j0 + 64, jlim - 64);
+            if (o3 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[3]), i, j0 + 96, jlim - 96);
         }
     }
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((t & 31) == 0 && cnt) atomicAdd(a.count, (unsigned long long)cnt);
+}
+
+// canonical K-major core-matrix slot of 32-bit element k (0..7) of row r (the TF32 probe)
+__device__ __forceinline__ int slot(int64_t r, int k) {
+    return (int)(((r >> 3) * 64) + ((k >> 2) * 32) + ((r & 7) * 4) + (k & 3));
 }
 
 // ---------------------------------------------------------------- accumulation probe
@@ -420,23 +448,72 @@ __global__ void __launch_bounds__(kThreads) tc_tf32_probe_kernel(const float *x,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
 }
 
+// D = X Y^T for one 128 x 128 x 16 block with caller-given fp16 operands (row-major
+// 128 x 16 each) into an F16 accumulator, read back with the packed loads the filter
+// uses: the accumulator-rounding test (d: 128 x 128 fp16 bit patterns).
+__global__ void __launch_bounds__(kThreads) tc_f16_probe_kernel(const uint16_t *x, const uint16_t *y, uint16_t *d) {
+    __shared__ __align__(1024) uint16_t sx[128 * 16], sy[128 * 16];
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ uint32_t taddr;
+    const int t = threadIdx.x, warp = t >> 5;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        sx[slot16(t, k)] = x[t * 16 + k];
+        sy[slot16(t, k)] = y[t * 16 + k];
+    }
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&taddr)),
+                     "n"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = taddr;
+    if (t == 0) {
+        mma_f16(tmem, smem_desc((uint32_t)__cvta_generic_to_shared(sx)),
+                smem_desc((uint32_t)__cvta_generic_to_shared(sy)));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb)
+                     : "memory");
+    }
+    mbar_wait(mb, 0, nullptr);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+    for (int cg = 0; cg < kCols / 32; ++cg) {
+        uint32_t v[16];
+        ldtm16p(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cg * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            d[t * 128 + cg * 32 + 2 * c] = (uint16_t)(v[c] & 0xffffu);
+            d[t * 128 + cg * 32 + 2 * c + 1] = (uint16_t)(v[c] >> 16);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+}
+
 }  // namespace
 
 namespace tri {
 
-#ifndef TRI_TC_FMUL
-#define TRI_TC_FMUL 1
-#endif
-constexpr int kFmul = TRI_TC_FMUL;   // values of each 32 tested on the FMA pipe (A/B'd on B200)
-
-size_t collide_tc_ws_bytes(const tri_map_t &m) { return (size_t)m.m * (size_t)m.rho * 64u; }
+size_t collide_tc_ws_bytes(const tri_map_t &m) { return (size_t)kHdrBytes + (size_t)m.m * (size_t)m.rho * 64u; }
 
 template <int kRho, bool kBB>
 static void launch_rho(const tri_map_t &m, TcArgs a, cudaStream_t st) {
     // pad the dynamic smem so at most kCtasPerSm CTAs share an SM (their TMEM columns fit)
     const int pad = 228 * 1024 / (kCtasPerSm + 1) + 1024;
     const int smem = 2 * kRho * 32 > pad ? 2 * kRho * 32 : pad;
-    auto k = collide_tc_kernel<kRho, kBB, kFmul>;
+    auto k = collide_tc_kernel<kRho, kBB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), kThreads, smem, st>>>(a);
     else k<<<tile_grid(a.omega_end - a.omega_begin), kThreads, smem, st>>>(a);
@@ -448,14 +525,19 @@ tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph,
     if (strategy == TRI_BB_TC && m.m > 65535) return TRI_EINVAL;
     TcArgs a;
     a.sph = (const float4 *)sph;
-    a.ops = (const uint32_t *)ws;
+    a.ops = (const uint16_t *)((const uint8_t *)ws + kHdrBytes);
     a.n = m.n;
     a.npad = m.m * (int64_t)m.rho;
     a.omega_begin = m.omega_begin;
     a.omega_end = m.omega_end;
     a.count = count;
-    collide_tc_prep<<<(unsigned)((a.npad + 255) / 256), 256, 0, st>>>(a.sph, a.n, a.npad, (uint32_t *)ws, count);
-    note_launches(1);
+    uint32_t *hdr = (uint32_t *)ws;
+    if (cudaMemsetAsync(hdr, 0, sizeof(uint32_t), st) != cudaSuccess) return TRI_ECUDA;
+    const int gb = (int)((a.n + 255) / 256 < 2 * (int64_t)sm_count() ? (a.n + 255) / 256 : 2 * sm_count());
+    collide_tc_bounds<<<gb > 0 ? gb : 1, 256, 0, st>>>(a.sph, a.n, hdr, count);
+    collide_tc_prep<<<(unsigned)((a.npad + 255) / 256), 256, 0, st>>>(a.sph, a.n, a.npad, hdr,
+                                                                      (uint16_t *)((uint8_t *)ws + kHdrBytes));
+    note_launches(2);
     if (a.omega_end > a.omega_begin) {
         const bool bb = strategy == TRI_BB_TC;
         if (m.rho == 1024) bb ? launch_rho<1024, true>(m, a, st) : launch_rho<1024, false>(m, a, st);
@@ -472,6 +554,12 @@ tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph,
 
 tri_status launch_tc_tf32_probe(const float *x, const float *y, float *d, cudaStream_t st) {
     tc_tf32_probe_kernel<<<1, kThreads, 0, st>>>(x, y, d);
+    note_launches(1);
+    return cuda_status();
+}
+
+tri_status launch_tc_f16_probe(const void *x, const void *y, void *d, cudaStream_t st) {
+    tc_f16_probe_kernel<<<1, kThreads, 0, st>>>((const uint16_t *)x, (const uint16_t *)y, (uint16_t *)d);
     note_launches(1);
     return cuda_status();
 }

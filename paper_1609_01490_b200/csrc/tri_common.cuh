@@ -292,6 +292,7 @@ tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph,
                              void *ws, cudaStream_t st);
 size_t collide_tc_ws_bytes(const tri_map_t &m);
 tri_status launch_tc_tf32_probe(const float *x, const float *y, float *d, cudaStream_t st);
+tri_status launch_tc_f16_probe(const void *x, const void *y, void *d, cudaStream_t st);
 tri_status launch_collide1d(const tri_map_t &m, int strategy, const float *iv, unsigned long long *count,
                             cudaStream_t st);
 tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_t *in, uint8_t *out,

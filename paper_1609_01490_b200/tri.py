@@ -75,6 +75,7 @@ SIGNATURES = {
     "tri_collide": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp], c_i32),
     "tri_collide_workspace_size": ([ctypes.POINTER(TriMap), c_i32], c_sz),
     "tri_tc_tf32_probe": ([c_vp, c_vp, c_vp, c_vp], c_i32),
+    "tri_tc_f16_probe": ([c_vp, c_vp, c_vp, c_vp], c_i32),
     "tri_ca_workspace_size": ([ctypes.POINTER(TriMap)], c_sz),
     "tri_ca_step": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp],
                     c_i32),
@@ -282,6 +283,15 @@ def tri_tc_tf32_probe(x, y, d, stream=None):
               "tri_tc_tf32_probe: contiguous float32 CUDA tensors")
     _need(x.numel() == 1024 and y.numel() == 1024 and d.numel() == 16384, "tri_tc_tf32_probe: 128x8, 128x8, 128x128")
     _ok(lib().tri_tc_tf32_probe(_ptr(x), _ptr(y), _ptr(d), _stream(stream)), "tri_tc_tf32_probe")
+
+
+def tri_tc_f16_probe(x, y, d, stream=None):
+    """Test hook: d (128 x 128 fp16) = x (128 x 16 fp16) @ y (128 x 16 fp16)^T on one tcgen05
+    kind::f16 MMA into an F16 accumulator."""
+    for t in (x, y, d):
+        _need(t.is_cuda and t.element_size() == 2 and t.is_contiguous(), "tri_tc_f16_probe: contiguous 16-bit CUDA")
+    _need(x.numel() == 2048 and y.numel() == 2048 and d.numel() == 16384, "tri_tc_f16_probe: 128x16, 128x16, 128x128")
+    _ok(lib().tri_tc_f16_probe(_ptr(x), _ptr(y), _ptr(d), _stream(stream)), "tri_tc_f16_probe")
 
 
 def tri_collide(m: TriMap, strategy, spheres, count, stream=None, ws=None):

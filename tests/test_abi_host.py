@@ -29,7 +29,8 @@ def header_functions():
 
 def test_header_parses():
     fns = header_functions()
-    for must in ("tri_map_init", "tri_dummy", "tri_edm", "tri_collide", "tri_ca_step", "tet_triplet"):
+    for must in ("tri_map_init", "tri_dummy", "tri_edm", "tri_collide", "tri_ca_step", "tet_triplet",
+                 "tri_tc_tf32_probe", "tri_tc_f16_probe", "tri_collide_workspace_size"):
         assert must in fns
 
 
@@ -279,7 +280,7 @@ def test_collide_triplet_ca_capacities(L):
     # the tensor-core strategies need their workspace: m * rho * 64 bytes
     mt = tri.tri_map_init(n, 384)
     need = L.tri_collide_workspace_size(ctypes.byref(mt), 8)
-    assert need == mt.m * 384 * 64 and L.tri_collide_workspace_size(ctypes.byref(mt), 0) == 0
+    assert need == 256 + mt.m * 384 * 64 and L.tri_collide_workspace_size(ctypes.byref(mt), 0) == 0
     for strat in (8, 9):
         assert L.tri_collide(ctypes.byref(mt), strat, vp(1 << 20), 16 * n, vp(2 << 20), 8, vp(3 << 20), need - 16,
                              None) == tri.TRI_EINVAL

@@ -37,9 +37,9 @@ def spheres():
     return torch.from_numpy(inputs.spheres(200000, 42, 0.01)).cuda()
 
 
-# bench.py: SIMT filter at rho = 256 (lambda / persist / BB), tcgen05 at rho = 1024 (lambda / BB)
-@pytest.mark.parametrize("strategy,rho", [("lambda", 256), ("persist", 256), ("bb", 256), ("tc", 1024),
-                                          ("bb_tc", 1024), ("tc", 256), ("tc", 512), ("tc", 768)])
+# bench.py: SIMT filter at rho = 256 (lambda / persist / BB), tcgen05 at rho = 768 (lambda / BB)
+@pytest.mark.parametrize("strategy,rho", [("lambda", 256), ("persist", 256), ("bb", 256), ("tc", 768),
+                                          ("bb_tc", 768), ("tc", 256), ("tc", 512), ("tc", 1024)])
 def test_collide_full_size_golden(spheres, strategy, rho):
     m = tri.tri_map_init(200000, rho, 1, 0, 1, 0)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")

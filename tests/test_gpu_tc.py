@@ -85,6 +85,46 @@ def test_tc_tf32_accumulation_bound(case):
     assert np.all(err <= 2.0 ** -20 * ab), ratio
 
 
+def f16(a):
+    return np.asarray(a, np.float64).astype(np.float16)
+
+
+@pytest.mark.parametrize("case", ["cancel_unit", "cancel_large", "cancel_tiny", "random", "filter_shape"])
+def test_tc_f16_accumulator_rounding(case):
+    """The filter's sign test reads an F16 accumulator: it assumes D = round_f16(wide sum)
+    -- products exact, summed in >= fp32 precision (within 2^-20 sum |x_k y_k| of the exact
+    sum), rounded once to nearest (overflow to +-inf).  Then D's sign is the exact sum's
+    whenever |exact| > 2^-20 sum |terms| and the rounding does not reach zero."""
+    rng = np.random.default_rng(11)
+    A = np.zeros((128, 16)); B = np.zeros((128, 16))
+    if case == "random":
+        A, B = rng.uniform(-2, 2, (128, 16)), rng.uniform(-2, 2, (128, 16))
+    else:
+        sc = {"cancel_unit": 0.5, "cancel_large": 60.0, "cancel_tiny": 0.01, "filter_shape": 0.5}[case]
+        x = f16(rng.uniform(-sc, sc, (128, 3))).astype(np.float64)
+        y = f16(x[rng.permutation(128)] + rng.normal(0, 1e-3 * sc, (128, 3))).astype(np.float64)
+        y[:64] = x[:64]
+        P, Q = (x ** 2).sum(1), (y ** 2).sum(1)
+        P1 = f16(P).astype(np.float64); P2 = f16((P - P1) * 2048).astype(np.float64)
+        Q1 = f16(Q).astype(np.float64); Q2 = f16((Q - Q1) * 2048).astype(np.float64)
+        S = 32768.0 if case == "filter_shape" else 1.0          # the filter's column scale
+        A[:, :3], A[:, 3], A[:, 4], A[:, 5], A[:, 6] = x, P1, P2, 1, 1 / 2048
+        B[:, :3], B[:, 3], B[:, 4], B[:, 5], B[:, 6] = -2 * S * y, S, S / 2048, S * Q1, S * Q2
+    A, B = f16(A), f16(B)
+    d = torch.empty((128, 128), dtype=torch.int16, device="cuda")
+    tri.tri_tc_f16_probe(torch.from_numpy(A.view(np.int16)).cuda(), torch.from_numpy(B.view(np.int16)).cuda(), d)
+    torch.cuda.synchronize()
+    D = d.cpu().numpy().view(np.float16).astype(np.float64)
+    Ad, Bd = A.astype(np.float64), B.astype(np.float64)
+    ex = Ad @ Bd.T
+    ab = (np.abs(Ad)[:, None, :] * np.abs(Bd)[None, :, :]).sum(-1)
+    lo = f16(ex - 2.0 ** -20 * ab).astype(np.float64)            # round_f16 of the end points of
+    hi = f16(ex + 2.0 ** -20 * ab).astype(np.float64)            # the wide sum's error interval
+    assert np.all((D >= np.minimum(lo, hi)) & (D <= np.maximum(lo, hi)))
+    sure = np.abs(ex) > 2.0 ** -20 * ab + 2.0 ** -24
+    assert np.array_equal(np.signbit(D)[sure], (ex < 0)[sure])
+
+
 @pytest.mark.parametrize("strategy,rho", [("tc", 384), ("bb_tc", 256), ("tc", 512), ("tc", 1024), ("bb_tc", 1024)])
 def test_collide_tc_special_values(orc, strategy, rho):
     """NaN, infinite and huge coordinates or radii never break exactness: the filter
