@@ -439,29 +439,33 @@ def bench_collide(rank, world, pk):
     clk = pk["sm_max_mhz"] * 1e6
     # rooflines in the method's units: the pair test is ~10 FP32 ops (3 FADD,
     # FMUL, 2 FFMA, FADD, FMUL, FSETP, IADD); as a contraction its minimum is ONE K = 6 dot
-    # product (x, y, z, r, A, 1) = 12 flops.  The tcgen05 kernel executes K = 8 (16 flops).
+    # product (x, y, z, r, A, 1) = 12 flops.  The tcgen05 kernel runs kind::f16 MMAs with
+    # K = 16 (32 flops per pair executed) against the fp16 dense peak (= the measured bf16).
+    f16_peak = pk["bf16_tflops"]
     res["roofline"] = {"bound": "tensor", "achieved": round(12.0 * pairs / world / sec / 1e12, 1),
-                       "peak": round(tf32_peak(pk), 1), "unit": "TFLOP/s (tf32)",
-                       "frac": round(12.0 * pairs / world / sec / 1e12 / tf32_peak(pk), 4),
-                       "flops_per_pair": 12, "executed_flops_per_pair": 16,
-                       "kernel": f"collide_tc_kernel<{COLLIDE_TC_RHO}, lambda> (tcgen05)",
-                       "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (nominal tf32 : bf16)"}
+                       "peak": round(f16_peak, 1), "unit": "TFLOP/s (fp16)",
+                       "frac": round(12.0 * pairs / world / sec / 1e12 / f16_peak, 4),
+                       "flops_per_pair": 12, "executed_flops_per_pair": 32,
+                       "executed_frac": round(32.0 * pairs / world / sec / 1e12 / f16_peak, 4),
+                       "kernel": f"collide_tc_kernel<{COLLIDE_TC_RHO}, lambda> (tcgen05 kind::f16, F16 accumulator)",
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops (fp16 dense rate = bf16)"}
     res["roofline_method_alu"] = {"bound": "alu", "achieved": round(10.0 * pairs / world / sec / 1e12, 2),
                                   "peak": round(fp32_peak(pk), 2), "unit": "TFLOP/s (fp32 ops)",
                                   "frac": round(10.0 * pairs / world / sec / 1e12 / fp32_peak(pk), 4),
                                   "ops_per_pair": 10,
                                   "note": "the SIMT formulation's work: > 1 means the tensor cores do it"}
-    # what the tcgen05 kernel's epilogue actually spends per pair: 4 B of TMEM read, and
-    # half a 3-input LOP3 (two sign bits per ALU op, 64 ALU lanes per SM per clock)
-    tm = 4.0 * pairs / world / sec / 1e12
-    tm_peak = 950.0 * 148 * clk / 1e12
-    res["roofline_tmem"] = {"bound": "tmem", "achieved": round(tm, 1), "peak": round(tm_peak, 1), "unit": "TB/s",
-                            "frac": round(tm / tm_peak, 4), "bytes_per_pair": 4,
-                            "peak_source": "tools/probes/tmem_bw.cu: 950 B/clk/SM measured on B200"}
-    al = 0.5 * pairs / world / sec
+    # what the epilogue spends per pair: one TMEM cell read (a 16-bit accumulator value in a
+    # 32-bit column), and a quarter of a 3-input LOP3 (four sign bits per ALU op, 64 ALU
+    # lanes per SM per clock)
+    tm = pairs / world / sec / 1e12
+    tm_peak = 240.0 * 148 * clk / 1e12
+    res["roofline_tmem"] = {"bound": "tmem", "achieved": round(tm, 2), "peak": round(tm_peak, 2),
+                            "unit": "T cells/s", "frac": round(tm / tm_peak, 4), "cells_per_pair": 1,
+                            "peak_source": "tools/probes/tmem_bw.cu: ~240 cells/clk/SM measured on B200"}
+    al = 0.25 * pairs / world / sec
     al_peak = 148 * 64 * clk
     res["roofline_epilogue_alu"] = {"bound": "alu", "achieved": round(al / 1e12, 2), "peak": round(al_peak / 1e12, 2),
-                                    "unit": "T LOP3/s", "frac": round(al / al_peak, 4), "ops_per_pair": 0.5}
+                                    "unit": "T LOP3/s", "frac": round(al / al_peak, 4), "ops_per_pair": 0.25}
     simt = min(res["lambda_ms"], res["persist_ms"])
     res["roofline_simt"] = {"bound": "alu", "achieved": round(5.0 * pairs / world / (simt * 1e-3) / 1e12, 2),
                             "peak": round(fp32_peak(pk), 2), "unit": "TFLOP/s (fp32 ops)",
