@@ -54,7 +54,7 @@ def main():
         fn = lambda: tri.tri_ca_steps(m, a.strategy, a.k, x, y)
     elif w == "collide1d":
         n = a.n or 200000
-        m = tri.tri_map_init(n, 256)
+        m = tri.tri_map_init(n, a.rho or 256)
         x = torch.from_numpy(inputs.intervals(n, 42, 1e-5)).cuda()
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         fn = lambda: tri.tri_collide1d(m, a.strategy, x, cnt)
