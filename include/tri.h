@@ -289,6 +289,21 @@ tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, c
                             const uint8_t *d_halo_below, size_t below_bytes,
                             uint8_t *d_peer_above, uint8_t *d_peer_below, void *d_ws, void *stream);
 
+/* `steps` generations of the same rule over the whole domain (world = 1, diag = 1,
+ * rho = 240), bytes in, bytes out: the state is packed to bits once (cell (i, j) at bit
+ * T(i) + j), advanced 8 generations per launch on two packed buffers in d_ws
+ * (tri_ca_run_workspace_size bytes: 2 x ceil(D / 32) words, 256-byte rounded; 16-byte
+ * aligned) -- a tile loads its region's covering words, keeps the generations in
+ * registers, stores whole words and OR-merges the partial words it shares with a
+ * neighbouring tile or row (the launch's output buffer is zeroed first) -- and unpacked
+ * once.  d_in / d_out: the packed Eq. 1 uint8 {0,1} state, in_bytes, out_bytes >= D,
+ * 16-byte aligned, may alias.  Same result as steps / 8 calls of tri_ca_steps; 8x less
+ * HBM traffic per launch than the byte state. */
+size_t tri_ca_run_workspace_size(const tri_map_t *map);
+tri_status tri_ca_run(const tri_map_t *map, int32_t strategy, int64_t steps, const uint8_t *d_in,
+                      size_t in_bytes, uint8_t *d_out, size_t out_bytes, void *d_ws, size_t ws_bytes,
+                      void *stream);
+
 /* CUDA IPC for the peer buffers of tri_ca_steps_p2p (one process per GPU).
  * tri_ipc_handle: the TRI_IPC_HANDLE_BYTES-byte handle of the device allocation
  * holding d_ptr and d_ptr's offset in it (cudaIpcGetMemHandle on the allocation

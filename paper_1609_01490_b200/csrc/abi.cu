@@ -312,6 +312,22 @@ tri_status tri_ca_steps_p2p(const tri_map_t *map, int32_t strategy, int32_t k, c
                            (cudaStream_t)stream);
 }
 
+size_t tri_ca_run_workspace_size(const tri_map_t *map) {
+    if (bad_map(map)) return 0;
+    return ca_run_ws_bytes(*map);
+}
+
+tri_status tri_ca_run(const tri_map_t *map, int32_t strategy, int64_t steps, const uint8_t *d_in, size_t in_bytes,
+                      uint8_t *d_out, size_t out_bytes, void *d_ws, size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    if (bad_map(map) || bad_strategy(strategy) || !d_in || !d_out || !d_ws || steps < 0) return TRI_EINVAL;
+    if (!map->diag || map->world != 1 || map->rho != 240) return TRI_EINVAL;
+    if (in_bytes < map->cells || out_bytes < map->cells || ws_bytes < ca_run_ws_bytes(*map)) return TRI_EINVAL;
+    if ((((uintptr_t)d_in) | ((uintptr_t)d_out) | ((uintptr_t)d_ws)) & 15u) return TRI_EINVAL;
+    if (strategy == TRI_BB && map->m > 65535) return TRI_EINVAL;
+    return launch_ca_run(*map, strategy, steps, d_in, d_out, d_ws, (cudaStream_t)stream);
+}
+
 tri_status tri_ipc_handle(const void *d_ptr, void *handle, uint64_t *offset) {
     if (!d_ptr || !handle || !offset) return TRI_EINVAL;
     void *base = nullptr;

@@ -45,6 +45,17 @@ struct CaArgs {
     uint8_t *peer_above, *peer_below;
 };
 
+#ifndef TRI_CA_PACKED_EXCH
+#define TRI_CA_PACKED_EXCH 1
+#endif
+// tri_ca_run's bit-packed state: cell (i, j) at bit T(i) + j of the word array.
+struct PackedArgs {
+    const uint32_t *in;
+    uint32_t *out;
+    int64_t n, k, nwords;
+    uint64_t omega_begin, omega_end;
+};
+
 // Row pointer to column 0 of row r, or nullptr for a dead row.
 __device__ __forceinline__ const uint8_t *row_ptr(const CaArgs &a, int64_t r) {
     if (r < 0 || r >= a.n) return nullptr;
@@ -638,14 +649,15 @@ __device__ __forceinline__ uint32_t tri_mask(int64_t r, int64_t n, int64_t cb) {
 //       phase-B lane idles (4 threads per band, 8 bands per warp), and the word
 //       pair a thread owns halves the shuffles per cell (the inner neighbour bits
 //       come from the thread's own other word).
-template <int RHO_, int NWV, int WPT_, int KMAX_>
+template <int RHO_, int NWV, int WPT_, int KMAX_, int SPILL_ = 15>
 struct Multi {
     static constexpr int RHO = RHO_;
     static constexpr int NW = NWV;
     static constexpr int WPT = WPT_;
     static constexpr int KMAX = KMAX_;
-    // garbage from the right edge reaches column c0 + 32 NW - 2K; phase C reads up to c0 + rho + 14
-    static_assert(32 * NW - 2 * KMAX >= RHO + 15, "bitmap too narrow for KMAX");
+    // garbage from the right edge reaches column c0 + 32 NW - 2K; the byte store phase reads
+    // up to c0 + rho + 14 (SPILL = 15), the bit-packed one up to c0 + rho - 1 (SPILL = 0)
+    static_assert(32 * NW - 2 * KMAX >= RHO + SPILL_, "bitmap too narrow for KMAX");
     static_assert(NW % WPT == 0 && RHO % 16 == 0, "geometry");
     static constexpr int NINMAX = RHO + 2 * KMAX;          // region rows
     static constexpr int TPB = NW / WPT;                   // threads per band
@@ -665,73 +677,18 @@ struct Multi {
     static constexpr int AW = NW | 1;                      // odd row stride: phase A's row-per-lane stores conflict-free
     struct Smem {
         uint32_t A[NINMAX][AW];                            // packed region (phase A) / final state (phase C)
-        uint32_t top[2][NBAND][NW], bot[2][NBAND][NW];     // band edge rows, double-buffered by generation
+        uint2 top[2][NBAND][NW], bot[2][NBAND][NW];        // band edge row sums (s0, s1), double-buffered
         uint64_t seg[RHO];
     };
 
-// P2P: the slice's first / last k rows also go to the neighbours' halo buffers (peer
-// memory); a compile-time flag so the plain launch carries none of that logic.
-template <bool P2P>
-static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
+// ---- B (shared by the byte and the bit-packed tile forms): K generations on the region
+// bitmap sm.A (rows r0 - K .., bit x <-> column cs + x); the result is left in sm.A.
+template <bool EXCH>
+static __device__ __forceinline__ void phase_b(const int64_t n, const int K, const int NIN, const int64_t r0,
+                                               const int64_t cs, Smem &sm) {
     const int t = threadIdx.x;
-    const int K = (int)a.k;
-    const int NIN = RHO + 2 * K;
-    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-    const int64_t cs = c0 - K;                        // column of bitmap bit 0
-    // ---- A: load + pack rows r0-K .. r0+RHO+K-1 (thread t = input row t): the
-    // row's 16-byte-aligned window straight into registers (read-only path),
-    // bytes outside the row masked before packing.  (Per-row cp.async.bulk
-    // copies serialise on the uniform datapath -- one ELECT/R2UR round per lane
-    // -- which made staging 40 % of the tile time.)
-    if (t < NIN) {
-        const int64_t r = r0 - K + t;
-        if (t >= K && t < K + RHO) sm.seg[t - K] = tri::T2((uint64_t)r) + (uint64_t)c0 - a.base;
-        const uint8_t *p = row_ptr(a, r);
-        if (!p) {
-#pragma unroll
-            for (int v = 0; v < NW; ++v) sm.A[t][v] = 0u;
-        } else {
-            const uintptr_t Ad = (uintptr_t)(p + cs);
-            const uint32_t e = (uint32_t)(Ad & 15u);
-            const int64_t col0 = cs - (int64_t)e;
-            const uint4 *q = (const uint4 *)(Ad & ~(uintptr_t)15);
-            if (col0 >= 0 && col0 + RAWB - 1 <= r) {
-                // whole window inside the row (hence inside the triangle): no masks
-                uint4 c[NCH];
-#pragma unroll
-                for (int h = 0; h < NCH; ++h) c[h] = __ldg(q + h);
-                uint32_t prev = bits::pack32(c[0], c[1]);
-#pragma unroll
-                for (int v = 1; v <= NW; ++v) {
-                    const uint32_t P = bits::pack32(c[2 * v], c[2 * v + 1]);
-                    sm.A[t][v - 1] = __funnelshift_r(prev, P, e);
-                    prev = P;
-                }
-            } else {
-                uint4 c[NCH];
-#pragma unroll
-                for (int h = 0; h < NCH; ++h) {
-                    const int64_t cb = col0 + 16 * h;
-                    const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
-                    c[h] = make_uint4(0, 0, 0, 0);
-                    if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
-                        c[h] = __ldg(q + h);
-                        bits::mask_chunk(c[h], lo_c, hi_c);
-                    }
-                }
-                uint32_t prev = 0;
-#pragma unroll
-                for (int v = 0; v <= NW; ++v) {
-                    const uint32_t P = bits::pack32(c[2 * v], c[2 * v + 1]);
-                    if (v > 0)
-                        sm.A[t][v - 1] = __funnelshift_r(prev, P, e) & tri_mask(r, a.n, cs + 32 * (v - 1));
-                    prev = P;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    // ---- B: K generations with the state in registers.  Thread (band, w) owns
+    struct { int64_t n; } a{n};
+    // K generations with the state in registers.  Thread (band, w) owns
     // bitmap word w of region rows [RB band, RB band + RB); horizontal neighbour
     // words come by shuffle (lane +-1), the rows above / below the band through
     // shared memory (one exchange per generation).  What enters at the region
@@ -796,25 +753,50 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
 #pragma unroll 1
             for (int g = 0; g < K; ++g) {
                 const int pb = g & 1;
-                if (live) {
+                uint32_t h0[RB + 2][WPT], h1[RB + 2][WPT], p0[RB][WPT], p1[RB][WPT];
+                if constexpr (EXCH) {
+                    // own rows' sums first; the band's first / last row sums go to the
+                    // neighbouring bands (which would otherwise recompute them: 2 of every
+                    // RB + 2 row sums)
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) hsum(X[q], h0[q + 1], h1[q + 1], p0[q], p1[q], true);
+                    if (live) {
+#pragma unroll
+                        for (int u = 0; u < WPT; ++u) {
+                            sm.top[pb][band][w0 + u] = make_uint2(h0[1][u], h1[1][u]);
+                            sm.bot[pb][band][w0 + u] = make_uint2(h0[RB][u], h1[RB][u]);
+                        }
+                    }
+                    __syncthreads();
 #pragma unroll
                     for (int u = 0; u < WPT; ++u) {
-                        sm.top[pb][band][w0 + u] = X[0][u];
-                        sm.bot[pb][band][w0 + u] = X[RB - 1][u];
+                        const uint2 up = (live && band > 0) ? sm.bot[pb][band - 1][w0 + u] : make_uint2(0u, 0u);
+                        const uint2 dn =
+                            (live && band + 1 < NBAND) ? sm.top[pb][band + 1][w0 + u] : make_uint2(0u, 0u);
+                        h0[0][u] = up.x; h1[0][u] = up.y;
+                        h0[RB + 1][u] = dn.x; h1[RB + 1][u] = dn.y;
                     }
-                }
-                __syncthreads();
-                uint32_t up[WPT], dn[WPT];
+                } else {
+                    // the band's edge rows go to the neighbouring bands, which form their sums
+                    if (live) {
 #pragma unroll
-                for (int u = 0; u < WPT; ++u) {
-                    up[u] = (live && band > 0) ? sm.bot[pb][band - 1][w0 + u] : 0u;
-                    dn[u] = (live && band + 1 < NBAND) ? sm.top[pb][band + 1][w0 + u] : 0u;
-                }
-                uint32_t h0[RB + 2][WPT], h1[RB + 2][WPT], p0[RB][WPT], p1[RB][WPT], u0[WPT], u1[WPT];
-                hsum(up, h0[0], h1[0], u0, u1, false);
+                        for (int u = 0; u < WPT; ++u) {
+                            sm.top[pb][band][w0 + u].x = X[0][u];
+                            sm.bot[pb][band][w0 + u].x = X[RB - 1][u];
+                        }
+                    }
+                    __syncthreads();
+                    uint32_t up[WPT], dn[WPT], u0[WPT], u1[WPT];
 #pragma unroll
-                for (int q = 0; q < RB; ++q) hsum(X[q], h0[q + 1], h1[q + 1], p0[q], p1[q], true);
-                hsum(dn, h0[RB + 1], h1[RB + 1], u0, u1, false);
+                    for (int u = 0; u < WPT; ++u) {
+                        up[u] = (live && band > 0) ? sm.bot[pb][band - 1][w0 + u].x : 0u;
+                        dn[u] = (live && band + 1 < NBAND) ? sm.top[pb][band + 1][w0 + u].x : 0u;
+                    }
+                    hsum(up, h0[0], h1[0], u0, u1, false);
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) hsum(X[q], h0[q + 1], h1[q + 1], p0[q], p1[q], true);
+                    hsum(dn, h0[RB + 1], h1[RB + 1], u0, u1, false);
+                }
 #pragma unroll
                 for (int q = 0; q < RB; ++q) {
 #pragma unroll
@@ -847,6 +829,71 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
         }
         __syncthreads();
     }
+}
+
+// P2P: the slice's first / last k rows also go to the neighbours' halo buffers (peer
+// memory); a compile-time flag so the plain launch carries none of that logic.
+template <bool P2P>
+static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
+    const int t = threadIdx.x;
+    const int K = (int)a.k;
+    const int NIN = RHO + 2 * K;
+    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
+    const int64_t cs = c0 - K;                        // column of bitmap bit 0
+    // ---- A: load + pack rows r0-K .. r0+RHO+K-1 (thread t = input row t): the
+    // row's 16-byte-aligned window straight into registers (read-only path),
+    // bytes outside the row masked before packing.  (Per-row cp.async.bulk
+    // copies serialise on the uniform datapath -- one ELECT/R2UR round per lane
+    // -- which made staging 40 % of the tile time.)
+    if (t < NIN) {
+        const int64_t r = r0 - K + t;
+        if (t >= K && t < K + RHO) sm.seg[t - K] = tri::T2((uint64_t)r) + (uint64_t)c0 - a.base;
+        const uint8_t *p = row_ptr(a, r);
+        if (!p) {
+#pragma unroll
+            for (int v = 0; v < NW; ++v) sm.A[t][v] = 0u;
+        } else {
+            const uintptr_t Ad = (uintptr_t)(p + cs);
+            const uint32_t e = (uint32_t)(Ad & 15u);
+            const int64_t col0 = cs - (int64_t)e;
+            const uint4 *q = (const uint4 *)(Ad & ~(uintptr_t)15);
+            if (col0 >= 0 && col0 + RAWB - 1 <= r) {
+                // whole window inside the row (hence inside the triangle): no masks
+                uint4 c[NCH];
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) c[h] = __ldg(q + h);
+                uint32_t prev = bits::pack32(c[0], c[1]);
+#pragma unroll
+                for (int v = 1; v <= NW; ++v) {
+                    const uint32_t P = bits::pack32(c[2 * v], c[2 * v + 1]);
+                    sm.A[t][v - 1] = __funnelshift_r(prev, P, e);
+                    prev = P;
+                }
+            } else {
+                uint4 c[NCH];
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) {
+                    const int64_t cb = col0 + 16 * h;
+                    const int64_t lo_c = cb < 0 ? -cb : 0, hi_c = r - cb + 1;
+                    c[h] = make_uint4(0, 0, 0, 0);
+                    if (lo_c < 16 && hi_c > 0 && lo_c < hi_c) {
+                        c[h] = __ldg(q + h);
+                        bits::mask_chunk(c[h], lo_c, hi_c);
+                    }
+                }
+                uint32_t prev = 0;
+#pragma unroll
+                for (int v = 0; v <= NW; ++v) {
+                    const uint32_t P = bits::pack32(c[2 * v], c[2 * v + 1]);
+                    if (v > 0)
+                        sm.A[t][v - 1] = __funnelshift_r(prev, P, e) & tri_mask(r, a.n, cs + 32 * (v - 1));
+                    prev = P;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    phase_b<false>(a.n, K, NIN, r0, cs, sm);
     uint32_t (*fin)[AW] = sm.A;
     // ---- C: aligned-chunk ownership (a 16-byte chunk is written by the tile
     // holding its first cell; the region covers the <= 15-column spill past the
@@ -935,11 +982,92 @@ static __device__ __forceinline__ void tile(const CaArgs &a, uint32_t bi, uint32
     if (P2P) __threadfence_system();
 }
 
+
+// ---- the bit-packed form (tri_ca_run): the state lives in HBM as packed bits, cell (i, j) at
+// bit T(i) + j (32 cells per 32-bit word).  A: each region row's NW + 1 covering words, one
+// funnel shift, the triangle mask; B: as above; C: the tile's row segments as whole words
+// (plain stores) and at most two partial words per row (atomicOr into a zeroed buffer: a
+// partial word's other bits belong to the neighbouring tile or row).
+static __device__ __forceinline__ void tile_packed(const PackedArgs &a, uint32_t bi, uint32_t bj, Smem &sm) {
+    const int t = threadIdx.x;
+    const int K = (int)a.k;
+    const int NIN = RHO + 2 * K;
+    const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
+    const int64_t cs = c0 - K;                        // column of bitmap bit 0
+    // CTA-uniform: every region cell inside the triangle and the domain -> no masks
+    const bool inside = cs >= 0 && cs + 32 * NW - 1 <= r0 - K && r0 + RHO + K <= a.n;
+    if (t < NIN) {
+        const int64_t r = r0 - K + t;
+        if (r < 0 || r >= a.n) {
+#pragma unroll
+            for (int v = 0; v < NW; ++v) sm.A[t][v] = 0u;
+        } else {
+            const int64_t b0 = (int64_t)tri::T2((uint64_t)r) + cs;          // bit of column cs (may be < 0)
+            const int64_t w0 = b0 >= 0 ? (b0 >> 5) : -((31 - b0) >> 5);      // floor(b0 / 32)
+            const uint32_t sh = (uint32_t)(b0 - 32 * w0);
+            uint32_t wd[NW + 1];
+            if (w0 >= 0 && w0 + NW < a.nwords) {
+#pragma unroll
+                for (int v = 0; v <= NW; ++v) wd[v] = __ldg(a.in + w0 + v);
+            } else {
+#pragma unroll
+                for (int v = 0; v <= NW; ++v) {
+                    const int64_t w = w0 + v;
+                    wd[v] = (w >= 0 && w < a.nwords) ? __ldg(a.in + w) : 0u;
+                }
+            }
+            if (inside) {
+#pragma unroll
+                for (int v = 0; v < NW; ++v) sm.A[t][v] = __funnelshift_r(wd[v], wd[v + 1], sh);
+            } else {
+#pragma unroll
+                for (int v = 0; v < NW; ++v)
+                    sm.A[t][v] = __funnelshift_r(wd[v], wd[v + 1], sh) & tri_mask(r, a.n, cs + 32 * v);
+            }
+        }
+    }
+    __syncthreads();
+    phase_b<TRI_CA_PACKED_EXCH>(a.n, K, NIN, r0, cs, sm);
+    uint32_t (*fin)[AW] = sm.A;
+    // C: one thread per tile row: the row segment's words, whole ones by plain stores, the
+    // partial first / last word by atomicOr (per-row set-up once, ~10 instructions a word)
+    for (int rr = t; rr < RHO; rr += NT) {
+        const int64_t r = r0 + rr;
+        if (r >= a.n) break;
+        const int64_t seg = r - c0 + 1;
+        if (seg <= 0) continue;
+        const int len = seg < RHO ? (int)seg : RHO;
+        const int64_t s = (int64_t)tri::T2((uint64_t)r) + c0;           // first bit of the segment
+        uint32_t *dst = a.out + (s >> 5);
+        int x = (int)(32 * (s >> 5) - s) + K;                           // bitmap bit of the word's bit 0
+        const uint32_t *row = fin[rr + K];
+        // first word: may start before the segment (x < K) -- bits below the segment masked off
+        {
+            const int off = x - K;                                      // in [-31, 0]
+            const uint32_t val = x >= 0 ? __funnelshift_r(row[x >> 5], row[(x >> 5) + 1], (uint32_t)(x & 31))
+                                        : row[0] << (uint32_t)(-x);
+            const int phi = len - off < 32 ? len - off : 32;
+            const uint32_t msk = (phi >= 32 ? 0xffffffffu : ((1u << phi) - 1u)) & ~((1u << (-off)) - 1u);
+            if (msk == 0xffffffffu) dst[0] = val;
+            else atomicOr(dst, val & msk);
+        }
+        int off = x - K + 32;
+        x += 32;
+#pragma unroll 1
+        for (int e = 1; off < len; ++e, off += 32, x += 32) {
+            const int wi = x >> 5;
+            const uint32_t val = __funnelshift_r(row[wi], wi + 1 < NW ? row[wi + 1] : 0u, (uint32_t)(x & 31));
+            if (len - off >= 32) dst[e] = val;
+            else atomicOr(dst + e, val & ((1u << (len - off)) - 1u));
+        }
+    }
+}
 };
 
 using G5 = Multi<128, 5, 1, 8>;     // rho = 128, k <= 8
 using G6 = Multi<128, 6, 1, 16>;    // rho = 128, 9 <= k <= 16
 using G8 = Multi<224, 8, 2, 8>;     // rho = 224, k <= 8
+using G8P = Multi<240, 8, 2, 8, 0>; // rho = 240, k <= 8, bit-packed state only: 256 columns = rho + 2k
 
 // G5: 7 CTAs per SM (40 registers, a few spills) hide more of phase A's load
 // latency than 5 CTAs without spills: 0.270 -> 0.250 ms at K = 1, n = 32768.
@@ -1005,6 +1133,85 @@ tri_status launch_geom(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t 
 tri_status launch(const tri_map_t &m, int strategy, CaArgs a, cudaStream_t st) {
     if (m.rho == G8::RHO) return launch_geom<G8>(m, strategy, a, st);
     return a.k <= G5::KMAX ? launch_geom<G5>(m, strategy, a, st) : launch_geom<G6>(m, strategy, a, st);
+}
+
+
+#ifndef TRI_CA_PACKED_CTAS
+#define TRI_CA_PACKED_CTAS 3
+#endif
+template <class M, int STRAT>
+__global__ void __launch_bounds__(M::NT, TRI_CA_PACKED_CTAS) ca_packed_kernel(PackedArgs a) {
+    __shared__ __align__(16) typename M::Smem sm;
+    if (STRAT == TRI_BB) {
+        if (blockIdx.x > blockIdx.y) return;
+        M::tile_packed(a, blockIdx.y, blockIdx.x, sm);
+    } else if (STRAT == TRI_LAMBDA) {
+        const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (w >= a.omega_end) return;
+        uint32_t bi, bj;
+        tri::lambda_map(w, bi, bj);
+        M::tile_packed(a, bi, bj, sm);
+    } else {
+#pragma unroll 1
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) {
+            M::tile_packed(a, t.bi, t.bj, sm);
+            __syncthreads();
+        }
+    }
+}
+
+// bytes -> bits: word w = cells [32 w, 32 w + 32) of the packed triangle (cells >= D are 0)
+__global__ void ca_pack_kernel(const uint8_t *__restrict__ in, uint64_t cells, uint32_t *__restrict__ out,
+                               int64_t nwords) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwords) return;
+    const uint64_t c = 32ull * (uint64_t)w;
+    uint32_t v = 0;
+    if (c + 32 <= cells) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(in + c);
+        v = bits::pack32(__ldg(p), __ldg(p + 1));
+    } else {
+        for (uint64_t e = 0; c + e < cells; ++e) v |= (uint32_t)(in[c + e] & 1u) << e;
+    }
+    out[w] = v;
+}
+
+// bits -> bytes {0, 1}
+__global__ void ca_unpack_kernel(const uint32_t *__restrict__ in, uint64_t cells, uint8_t *__restrict__ out,
+                                 int64_t nwords) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwords) return;
+    const uint64_t c = 32ull * (uint64_t)w;
+    const uint32_t v = __ldg(in + w);
+    if (c + 32 <= cells) {
+        uint4 *p = reinterpret_cast<uint4 *>(out + c);
+        p[0] = make_uint4(bits::spread4(v & 15u), bits::spread4((v >> 4) & 15u), bits::spread4((v >> 8) & 15u),
+                          bits::spread4((v >> 12) & 15u));
+        p[1] = make_uint4(bits::spread4((v >> 16) & 15u), bits::spread4((v >> 20) & 15u),
+                          bits::spread4((v >> 24) & 15u), bits::spread4(v >> 28));
+    } else {
+        for (uint64_t e = 0; c + e < cells; ++e) out[c + e] = (uint8_t)((v >> e) & 1u);
+    }
+}
+
+template <class M>
+tri_status launch_packed(const tri_map_t &m, int strategy, PackedArgs a, cudaStream_t st) {
+    constexpr int NT = M::NT;
+    if (strategy == TRI_BB) {
+        if (m.m > 65535) return TRI_ENOTSUP;
+        ca_packed_kernel<M, TRI_BB><<<dim3((unsigned)m.m, (unsigned)m.m), NT, 0, st>>>(a);
+    } else if (strategy == TRI_LAMBDA) {
+        ca_packed_kernel<M, TRI_LAMBDA><<<tri::tile_grid(a.omega_end - a.omega_begin), NT, 0, st>>>(a);
+    } else {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ca_packed_kernel<M, TRI_LAMBDA_PERSIST>, NT, 0);
+        uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
+        const uint64_t nb = a.omega_end - a.omega_begin;
+        if (g > nb) g = nb;
+        ca_packed_kernel<M, TRI_LAMBDA_PERSIST><<<(unsigned)g, NT, 0, st>>>(a);
+    }
+    tri::note_launches(1);
+    return tri::cuda_status();
 }
 
 }  // namespace multi
@@ -1101,6 +1308,38 @@ tri_status launch_ca_steps(const tri_map_t &m, int strategy, int k, const uint8_
     a.omega_begin = m.omega_begin; a.omega_end = m.omega_end;
     a.tile_row_begin = 0;
     return multi::launch(m, strategy, a, st);
+}
+
+
+size_t ca_run_ws_bytes(const tri_map_t &m) {
+    const uint64_t nwords = (m.cells + 31) / 32;
+    return (size_t)(2 * ((nwords * 4 + 255) / 256 * 256));
+}
+
+// steps generations at rho = 240, 8 per launch, on two packed buffers in the workspace
+tri_status launch_ca_run(const tri_map_t &m, int strategy, int64_t steps, const uint8_t *in, uint8_t *out,
+                         void *ws, cudaStream_t st) {
+    const int64_t nwords = (int64_t)((m.cells + 31) / 32);
+    const size_t half = (size_t)((nwords * 4 + 255) / 256 * 256);
+    uint32_t *buf[2] = {(uint32_t *)ws, (uint32_t *)((uint8_t *)ws + half)};
+    const unsigned g = (unsigned)((nwords + 255) / 256);
+    multi::ca_pack_kernel<<<g, 256, 0, st>>>(in, m.cells, buf[0], nwords);
+    int cur = 0;
+    for (int64_t done = 0; done < steps;) {
+        const int64_t k = steps - done < multi::G8P::KMAX ? steps - done : multi::G8P::KMAX;
+        if (cudaMemsetAsync(buf[cur ^ 1], 0, (size_t)nwords * 4, st) != cudaSuccess) return TRI_ECUDA;
+        PackedArgs a;
+        a.in = buf[cur]; a.out = buf[cur ^ 1];
+        a.n = m.n; a.k = k; a.nwords = nwords;
+        a.omega_begin = 0; a.omega_end = m.blocks;
+        const tri_status rc = multi::launch_packed<multi::G8P>(m, strategy, a, st);
+        if (rc != TRI_OK) return rc;
+        cur ^= 1;
+        done += k;
+    }
+    multi::ca_unpack_kernel<<<g, 256, 0, st>>>(buf[cur], m.cells, out, nwords);
+    note_launches(2);                                   // pack + unpack (launch_packed counts its own)
+    return cuda_status();
 }
 
 }  // namespace tri

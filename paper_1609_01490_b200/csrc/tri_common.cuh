@@ -273,6 +273,10 @@ inline dim3 tile_grid(uint64_t nb) {
     return dim3((unsigned)gx, (unsigned)(gy ? gy : 1), 1);
 }
 
+size_t ca_run_ws_bytes(const tri_map_t &m);
+tri_status launch_ca_run(const tri_map_t &m, int strategy, int64_t steps, const uint8_t *in, uint8_t *out,
+                         void *ws, cudaStream_t st);
+
 // Shared argument validation of tri_edm / tri_edm_host (abi.cu): true = EINVAL.
 bool edm_args_bad(const tri_map_t *map, int32_t strategy, int32_t dim, int64_t ld, size_t pts_bytes,
                   size_t out_bytes);

@@ -81,6 +81,8 @@ SIGNATURES = {
                     c_i32),
     "tri_ca_steps": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz,
                       c_vp, c_vp], c_i32),
+    "tri_ca_run_workspace_size": ([ctypes.POINTER(TriMap)], c_sz),
+    "tri_ca_run": ([ctypes.POINTER(TriMap), c_i32, c_i64, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp], c_i32),
     "tri_ca_steps_p2p": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_sz,
                           c_vp, c_vp, c_vp, c_vp], c_i32),
     "tri_ipc_handle": ([c_vp, c_vp, ctypes.POINTER(c_u64)], c_i32),
@@ -339,6 +341,21 @@ def _span(x):
     if x is None:
         return 0
     return (1 << 62) if isinstance(x, int) else x.numel() * x.element_size()
+
+
+def tri_ca_run_workspace_size(m: TriMap) -> int:
+    return int(lib().tri_ca_run_workspace_size(ctypes.byref(m)))
+
+
+def tri_ca_run(m: TriMap, strategy, steps, state_in, state_out, ws=None, stream=None):
+    """`steps` generations on the bit-packed state (world 1, rho = 240); bytes in, bytes out.
+    ws: tri_ca_run_workspace_size bytes of device memory (allocated here when None)."""
+    _u8(state_in, state_out)
+    if ws is None:
+        import torch
+        ws = torch.empty(tri_ca_run_workspace_size(m), dtype=torch.uint8, device=state_in.device)
+    _ok(lib().tri_ca_run(ctypes.byref(m), _strategy(strategy), int(steps), _ptr(state_in), _nbytes(state_in),
+                         _ptr(state_out), _nbytes(state_out), _ptr(ws), _nbytes(ws), _stream(stream)), "tri_ca_run")
 
 
 def _addr(x):

@@ -307,3 +307,24 @@ def test_collide_triplet_ca_capacities(L):
     sk = lambda ab: L.tri_ca_steps(ctypes.byref(mc), 0, k, vp(1 << 20), oc, vp(1 << 24), oc, vp(1 << 26), ab,
                                    None, 0, None, None)
     assert sk(T(R0) - T(R0 - k) - 1) == tri.TRI_EINVAL          # k rows above: T(R0) - T(R0 - k) bytes
+
+
+def test_ca_run_validation(L):
+    """tri_ca_run: world 1, rho 224, capacities, workspace, steps >= 0 -- EINVAL before any launch."""
+    import ctypes
+    vp = ctypes.c_void_p
+    n = 1000
+    m = tri.tri_map_init(n, 240)
+    D = n * (n + 1) // 2
+    ws = L.tri_ca_run_workspace_size(ctypes.byref(m))
+    assert ws == 2 * (((D + 31) // 32 * 4 + 255) // 256 * 256)
+    run = lambda mp, st=0, steps=5, ib=D, ob=D, wb=ws, w=vp(3 << 20): L.tri_ca_run(
+        ctypes.byref(mp), st, steps, vp(1 << 20), ib, vp(2 << 20), ob, w, wb, None)
+    assert run(m, ib=D - 1) == tri.TRI_EINVAL
+    assert run(m, ob=D - 1) == tri.TRI_EINVAL
+    assert run(m, wb=ws - 1) == tri.TRI_EINVAL
+    assert run(m, w=None) == tri.TRI_EINVAL
+    assert run(m, steps=-1) == tri.TRI_EINVAL
+    assert run(m, st=tri.TRI_LAMBDA_CLC) == tri.TRI_EINVAL
+    assert run(tri.tri_map_init(n, 224)) == tri.TRI_EINVAL                 # rho 240 only
+    assert run(tri.tri_map_init(n, 240, 1, 0, 2, 1)) == tri.TRI_EINVAL     # one rank only

@@ -92,6 +92,21 @@ def test_ca_single_step_plan_100_generations(strategy):
     assert got == (G["ca_n32768_seed42_g100_sha256"], int(G["ca_n32768_seed42_g100_alive"]))
 
 
+@pytest.mark.parametrize("strategy", ["lambda", "bb"])
+def test_ca_run_packed_100_generations(strategy):
+    """tri_ca_run, the bench's CA path: the bit-packed state, 13 launches of <= 8 generations."""
+    n = 32768
+    m = tri.tri_map_init(n, 240)
+    x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
+    y = torch.empty_like(x)
+    tri.tri_ca_run(m, strategy, 100, x, y)
+    torch.cuda.synchronize()
+    assert _digest(y) == (G["ca_n32768_seed42_g100_sha256"], int(G["ca_n32768_seed42_g100_alive"]))
+    tri.tri_ca_run(m, "lambda", 8, x, y)
+    torch.cuda.synchronize()
+    assert _digest(y) == (G["ca_n32768_seed42_g8_sha256"], int(G["ca_n32768_seed42_g8_alive"]))
+
+
 @pytest.mark.parametrize("rho,k", [(224, 8), (128, 8), (128, 1)])
 def test_ca_first_launch(rho, k):
     got = _ca_plan("lambda", rho, [k])

@@ -502,6 +502,42 @@ def test_ca_steps_rho224(orc, strategy, k, n, seed):
     assert np.array_equal(ca_steps_gpu(n, st, 2, k, strategy, rho=224), orc.ca_run(n, st, 2 * k))
 
 
+# ---- tri_ca_run: the bit-packed state (pack once, 8 generations per launch, unpack once)
+@pytest.mark.parametrize("strategy", ["lambda", "bb", "persist"])
+@pytest.mark.parametrize("n,seed,steps", [(1, 7, 3), (2, 42, 1), (31, 7, 9), (33, 42, 4), (224, 7, 8),
+                                          (225, 42, 17), (700, 7, 0), (700, 42, 1), (1000, 7, 13),
+                                          (2049, 42, 25), (4000, 7, 16)])
+def test_ca_run_packed(orc, strategy, n, seed, steps):
+    st = inputs.ca_state(n, seed)
+    m = tri.tri_map_init(n, 240)
+    x = torch.from_numpy(st).cuda()
+    y = torch.full_like(x, 0x77)
+    tri.tri_ca_run(m, strategy, steps, x, y)
+    sync()
+    assert np.array_equal(y.cpu().numpy(), orc.ca_run(n, st, steps))
+    assert np.array_equal(x.cpu().numpy(), st)                   # the input is not modified
+
+
+def test_ca_run_packed_patterns_and_alias(orc):
+    """Glider, blinker, the diagonal L-triomino (still only because the cell that would
+    complete it is outside the triangle) on the packed state; input and output aliased."""
+    n = 300
+    st = np.zeros(T(n), np.uint8)
+    def put(i, j):
+        st[T(i) + j] = 1
+    for (i, j) in ((150, 40), (151, 41), (152, 39), (152, 40), (152, 41)):    # glider
+        put(i, j)
+    for (i, j) in ((200, 10), (200, 11), (200, 12)):                           # blinker
+        put(i, j)
+    for (i, j) in ((100, 100), (101, 100), (101, 101)):                        # L-triomino
+        put(i, j)
+    x = torch.from_numpy(st).cuda()
+    m = tri.tri_map_init(n, 240)
+    tri.tri_ca_run(m, "lambda", 20, x, x)
+    sync()
+    assert np.array_equal(x.cpu().numpy(), orc.ca_run(n, st, 20))
+
+
 @pytest.mark.parametrize("world,k,rho", [(2, 4, 224), (3, 8, 224), (4, 3, 224)])
 def test_ca_steps_deep_halo_ranks_rho224(orc, world, k, rho):
     n = 2000
