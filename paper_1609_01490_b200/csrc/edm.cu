@@ -10,23 +10,28 @@
 // cells even when they run past the tile edge (EDM is pointwise, so the
 // neighbour cells are computable anywhere).
 //
-// Interior tiles (bj + 1 < bi: every chunk stays inside its row) take the
-// fast path: one warp walks ROWS rows of the tile, lane k owning chunk k
-// (rho = 32 CW, so each warp store is one contiguous 512 B / 1 KB run).  The
-// row's chunk phase delta = (-T(i)) mod CW is warp-uniform, so every lane takes
-// its CW columns from a (2 CW - 1)-column register window through a uniform
-// branch; the row offset is advanced incrementally (T(i+1) = T(i) + i + 1) and
-// the row point is broadcast by shuffle.  Tiles touching the diagonal
-// (bj >= bi - 1) take a checked path that walks Eq. 1 across row ends and the
-// slice end.  (A packed-f32x2 interior path -- two cells per FADD2/FMUL2/FFMA2 --
-// was measured: 1.386 -> 1.296 ms per isolated launch, but 1.40 -> 1.46 ms per
-// step in the bench's 200-launch sustained loop; the same store pattern with no
-// arithmetic at all is slower still there (1.47 ms): the packed layout's write
-// stream, not instruction issue, sets the pace, so the scalar path stays.  Round 2
-// measured the same for row points from shared memory instead of shuffles, and for 32-B
-// chunks at rho = 128 with two rows per warp store (1.40 -> 1.80 ms); 5 CTAs per SM
-// (<= 48 registers) and float4 point loads for 4 features take the paper's 4-D EDM
-// from 2.59 to 1.55 ms.)
+// rho = 128 (the bench): ownership is per aligned 128-BYTE LINE instead (OwnW), so
+// every warp store is 4 whole L2 lines.  A 512-B store at a 16-B phase touches 5
+// lines, 2 of them partially, and that alone costs the write stream ~20 %
+// (tools/probes/line_align.cu: 7.18 vs 5.93 TB/s for the same tiles with constant
+// data).  Interior tiles (bj + 1 < bi: every line stays inside its row) take the fast
+// path edm_tile_interior_line: column points staged once per tile in shared memory as
+// four rotated SoA copies (one aligned LDS.128 per coordinate per lane at any phase),
+// row points as float4s, rows i and i + 64 (same phase) walked as a pair so one set of
+// column loads serves 8 cells per lane, two cells per FADD2/FMUL2/FFMA2; 4 CTAs per SM.
+// Round 2 measured 1.39 -> 1.28 ms per step in the bench's sustained loop (n = 65536,
+// 3-D) and 1.55 -> 1.27 ms for 4 features; single rows with shared-memory columns and
+// scalar math were slower than the chunk form (1.55 vs 1.47 ms: more instructions
+// under the board's power cap), 5 CTAs per SM within noise of 4, 3 / 2 CTAs slower.
+//
+// Other tile edges: interior tiles walk ROWS rows per warp, lane k owning chunk k
+// (rho = 32 CW, so each warp store is one contiguous 512 B / 1 KB run); the row's
+// chunk phase delta = (-T(i)) mod CW is warp-uniform, so every lane takes its CW
+// columns from a (2 CW - 1)-column register window through a uniform branch; the row
+// offset is advanced incrementally (T(i+1) = T(i) + i + 1) and the row point is
+// broadcast by shuffle.  Tiles touching the diagonal (bj >= bi - 1) take a checked
+// path that walks Eq. 1 across row ends and the slice end, honouring the same
+// ownership unit.
 #include "tri_common.cuh"
 
 namespace {
@@ -156,11 +161,138 @@ __device__ __forceinline__ void edm_tile_interior(const EdmArgs &a, int64_t r0, 
     }
 }
 
+// rho = 128 with TRI_EDM_LINE: ownership is per 128-byte LINE (32 floats) instead of per
+// 16-byte chunk.  Every aligned line of the output slice is written by the tile-row
+// segment holding its first cell, by one warp store per 4 lines, so no warp store
+// straddles a line boundary (a 512-B store at a 16-B phase touches 5 lines, 2 of them
+// partially; tools/probes/line_align.cu measures what that costs the write stream).
+#ifndef TRI_EDM_LINE
+#define TRI_EDM_LINE 1
+#endif
+template <int RHO> struct OwnW { static constexpr int OW = (RHO == 128 && TRI_EDM_LINE) ? 32 : ChunkW<RHO>::CW; };
+constexpr int kLineCols = 160;        // staged columns c0 + t (t < 160) per rotation: lanes reach 4 (31 + 7) + 3
+template <int DIM> struct LineSmem { static constexpr int FLOATS = 4 * DIM * kLineCols + 4 * 128; };
+
+// Interior tile, line ownership (rho = 128).  The row's line phase delta = (-T(i)) mod 32 =
+// 4a + b is warp-uniform; lane k writes cells delta + 4k .. + 3 of the segment, i.e. columns
+// c0 + 4(k + a) + b + e.  The tile's 163 column points are staged in shared memory as four
+// rotated SoA copies rot[b][d][t] = point (c0 + t + b), so every lane reads its 4 columns of
+// one coordinate with one aligned LDS.128 (a warp reads 512 contiguous bytes: 4 wavefronts),
+// and the tile's 128 row points as float4s (one broadcast LDS.128 per row).  Rows i and
+// i + 64 have the same phase (T(i + 64) - T(i) = 64 i + 2080 = 0 mod 32), so a warp walks
+// row PAIRS (i, i + 64): one set of column loads serves 8 cells per lane.
+// One row pair (i, i + 64) of a line-owned interior tile: lane's chunk at the row's phase.
+template <int DIM, bool SECOND>
+__device__ __forceinline__ void edm_line_pair(const float *rl, const float4 *rp, float *&pa_row, float *&pb_row,
+                                              uint32_t &s32, uint32_t &inc) {
+    const int delta = (int)((0u - s32) & 31u);
+    const float *src = rl + (delta & 3) * DIM * kLineCols + (delta & ~3);
+    const float4 pa = rp[0], pb = rp[64];
+    const float pav[4] = {pa.x, pa.y, pa.z, pa.w}, pbv[4] = {pb.x, pb.y, pb.z, pb.w};
+    unsigned long long a01 = 0, a23 = 0, b01 = 0, b23 = 0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(src + d * kLineCols);
+        unsigned long long e01, e23, f01, f23, pp, qq;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(pp) : "f"(pav[d]));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e01) : "l"(pp), "l"(w.x));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e23) : "l"(pp), "l"(w.y));
+        if (d == 0) {
+            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(a01) : "l"(e01));
+            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(a23) : "l"(e23));
+        } else {
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(a01) : "l"(e01));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(a23) : "l"(e23));
+        }
+        if constexpr (SECOND) {
+            asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(pbv[d]));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f01) : "l"(qq), "l"(w.x));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f23) : "l"(qq), "l"(w.y));
+            if (d == 0) {
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(b01) : "l"(f01));
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(b23) : "l"(f23));
+            } else {
+                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(b01) : "l"(f01));
+                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(b23) : "l"(f23));
+            }
+        }
+    }
+    float v[8];
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(a01));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(a23));
+    st_cs_v4(pa_row + delta, sqrt_approx(v[0]), sqrt_approx(v[1]), sqrt_approx(v[2]), sqrt_approx(v[3]));
+    if constexpr (SECOND) {
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[4]), "=f"(v[5]) : "l"(b01));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[6]), "=f"(v[7]) : "l"(b23));
+        st_cs_v4(pb_row + delta, sqrt_approx(v[4]), sqrt_approx(v[5]), sqrt_approx(v[6]), sqrt_approx(v[7]));
+    }
+    pa_row += inc;                                            // T(i + 1) = T(i) + i + 1
+    pb_row += inc + 64u;
+    s32 += inc;
+    ++inc;
+}
+
+template <int DIM, bool VEC4 = false>
+__device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t r0, int64_t c0, float *rot) {
+    constexpr int RHO = 128, PAIRS = RHO / 2 / kWarps;        // 8 row pairs per warp
+    float4 *rowp = reinterpret_cast<float4 *>(rot + 4 * DIM * kLineCols);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();                                          // the previous tile's readers are done
+    for (int t = threadIdx.x; t < kLineCols + 3 + RHO; t += kEdmThreads) {
+        const bool is_col = t < kLineCols + 3;
+        const int64_t pt = is_col ? c0 + t : r0 + (t - kLineCols - 3);   // col <= c0 + 162 < r0
+        if (!is_col && pt >= a.n) continue;
+        float q[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (VEC4) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(a.pts + pt * a.ld));
+            q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+        } else {
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) q[d] = __ldg(a.pts + pt * a.ld + d);
+        }
+        if (is_col) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (t - b >= 0 && t - b < kLineCols) {
+#pragma unroll
+                    for (int d = 0; d < DIM; ++d) rot[(b * DIM + d) * kLineCols + t - b] = q[d];
+                }
+        } else {
+            rowp[t - kLineCols - 3] = make_float4(q[0], q[1], q[2], q[3]);
+        }
+    }
+    __syncthreads();
+    const int64_t i0 = r0 + (int64_t)warp * PAIRS;            // first row of the pair walk
+    if (i0 >= a.n) return;
+    const uint64_t s0 = tri::T2((uint64_t)i0) + (uint64_t)c0 - a.out_offset;   // local start of row i0
+    float *pa_row = a.out + s0 + 4 * lane;                    // row i, lane's chunk at phase 0
+    float *pb_row = pa_row + (64u * (uint64_t)i0 + 2080u);    // row i + 64 (T(i + 64) - T(i))
+    uint32_t s32 = (uint32_t)s0;                              // low bits of the row start (phase)
+    const int na = (int)((a.n - i0) < PAIRS ? (a.n - i0) : PAIRS);              // rows i < n
+    const int nb = (int)((a.n - i0 - 64) < PAIRS ? ((a.n - i0 - 64) > 0 ? (a.n - i0 - 64) : 0) : PAIRS);
+    const float *rl = rot + 4 * lane;
+    const float4 *rp = rowp + warp * PAIRS;
+    uint32_t inc = (uint32_t)i0 + 1u;                         // T(i + 1) - T(i)
+    if (nb == PAIRS) {                                        // every row pair inside (all but the last tile row)
+#pragma unroll
+        for (int t = 0; t < PAIRS; ++t)
+            edm_line_pair<DIM, true>(rl, rp + t, pa_row, pb_row, s32, inc);
+    } else {
+#pragma unroll 1
+        for (int t = 0; t < na; ++t) {
+            if (t < nb) edm_line_pair<DIM, true>(rl, rp + t, pa_row, pb_row, s32, inc);
+            else edm_line_pair<DIM, false>(rl, rp + t, pa_row, pb_row, s32, inc);
+        }
+    }
+}
+
 // Any tile (used for tiles touching the diagonal, and for rho < 128): every
-// chunk slot of every row, cells walked along Eq. 1, all bounds checked.
+// chunk slot of every row, cells walked along Eq. 1, all bounds checked.  A slot belongs
+// to this segment when its ownership unit (OW floats: the chunk, or the 128-B line at
+// rho = 128) starts inside the segment; it may run past the segment / row end.
 template <int RHO, int DIM>
 __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, int64_t c0) {
-    constexpr int CW = ChunkW<RHO>::CW;
+    constexpr int CW = ChunkW<RHO>::CW, OW = OwnW<RHO>::OW;
     constexpr int L = RHO / CW;                       // chunk slots per row segment
     const int t = threadIdx.x;
 #pragma unroll 1
@@ -171,8 +303,9 @@ __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, i
         const uint64_t s = tri::T2((uint64_t)i) + (uint64_t)c0 - a.out_offset;
         const int64_t seg = i - c0 + 1;
         const int64_t len = seg < RHO ? seg : RHO;
-        const int off = (int)((0u - (uint32_t)s) & (uint32_t)(CW - 1)) + CW * k;
-        if (off >= len) continue;                      // chunk owned by the next segment
+        const int dl = (int)((0u - (uint32_t)s) & (uint32_t)(OW - 1));
+        const int off = dl + CW * k;
+        if (dl + (CW * k / OW) * OW >= len) continue;  // unit owned by the next segment
         const uint64_t c = s + (uint64_t)off;
         float v[CW];
         int64_t ii = i, jj = c0 + off;
@@ -194,9 +327,15 @@ __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, i
 }
 
 template <int RHO, int DIM>
-__device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj) {
+__device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t bj, float *rot) {
     const int64_t r0 = (int64_t)bi * RHO, c0 = (int64_t)bj * RHO;
-    if constexpr (RHO >= 128) {
+    if constexpr (OwnW<RHO>::OW == 32) {
+        if (bj + 1 < bi) {
+            if (DIM == 4 && a.vec4) edm_tile_interior_line<DIM, DIM == 4>(a, r0, c0, rot);
+            else edm_tile_interior_line<DIM>(a, r0, c0, rot);
+            return;
+        }
+    } else if constexpr (RHO >= 128) {
         if (bj + 1 < bi) {
             if (DIM == 4 && a.vec4) edm_tile_interior<RHO, DIM, DIM == 4>(a, r0, c0);
             else edm_tile_interior<RHO, DIM>(a, r0, c0);
@@ -207,18 +346,19 @@ __device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t
 }
 
 template <int RHO, int DIM, int STRAT>
-__global__ void __launch_bounds__(kEdmThreads, 5) edm_kernel(EdmArgs a) {
+__global__ void __launch_bounds__(kEdmThreads, 4) edm_kernel(EdmArgs a) {
+    __shared__ __align__(16) float rot[OwnW<RHO>::OW == 32 ? LineSmem<DIM>::FLOATS : 4];
     if (STRAT == TRI_BB) {
         const uint32_t bj = blockIdx.x;
         const uint32_t bi = blockIdx.y + (uint32_t)a.tile_row_begin;
         if (bj > bi) return;                                  // discard
-        edm_tile<RHO, DIM>(a, bi, bj);
+        edm_tile<RHO, DIM>(a, bi, bj, rot);
     } else if (STRAT == TRI_LAMBDA) {
         const uint64_t w = a.omega_begin + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
         if (w >= a.omega_end) return;
         uint32_t bi, bj;
         tri::lambda_map(w, bi, bj);
-        edm_tile<RHO, DIM>(a, bi, bj);
+        edm_tile<RHO, DIM>(a, bi, bj, rot);
     } else if (STRAT == TRI_LAMBDA_CLC) {
         __shared__ tri::ClcSched clc;
         if (threadIdx.x == 0) clc.init();
@@ -231,7 +371,7 @@ __global__ void __launch_bounds__(kEdmThreads, 5) edm_kernel(EdmArgs a) {
             if (w < a.omega_end) {
                 uint32_t bi, bj;
                 tri::lambda_map(w, bi, bj);
-                edm_tile<RHO, DIM>(a, bi, bj);
+                edm_tile<RHO, DIM>(a, bi, bj, rot);
             }
             const bool more = clc.receive(phase, bx, by);
             __syncthreads();                                  // handle read by all before the next request
@@ -239,7 +379,7 @@ __global__ void __launch_bounds__(kEdmThreads, 5) edm_kernel(EdmArgs a) {
         }
     } else {
 #pragma unroll 1
-        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) edm_tile<RHO, DIM>(a, t.bi, t.bj);
+        for (tri::TileWalk t(a.omega_begin, a.omega_end); t.more(); t.next()) edm_tile<RHO, DIM>(a, t.bi, t.bj, rot);
     }
 }
 
