@@ -1,7 +1,11 @@
 // ca.cu -- Life B3/S23 on the triangular domain {(i, j): 0 <= j <= i < n}
 // (P:79-80 names cellular automata on triangular domains, citing Conway's
 // Life; cells outside the triangle are dead -- DESIGN.md reading Q11).
-// State: u8 {0,1} in the packed Eq. 1 layout.  Three kernels:
+// State: u8 {0,1} in the packed Eq. 1 layout.  Four kernels:
+//   rho = 240: multi::ca_packed_kernel -- tri_ca_run (the bench's N = 1 path): the
+//              state converted once to BITS in the packed Eq. 1 order (bit T(i) + j),
+//              8 generations per launch on a register-resident bitmap, converted back
+//              at the end (8x less HBM traffic per launch than the byte state);
 //   rho = 128, 224: multi::ca_multi_kernel -- k generations per launch on a
 //              register-resident bitmap (tri_ca_steps; tri_ca_step is k = 1;
 //              tri_ca_steps_p2p also stores the halo rows into peer memory);
