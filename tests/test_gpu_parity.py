@@ -197,11 +197,12 @@ def test_edm_small(orc, strategy, rho, n, seed):
     edm_close(got[: m.out_cells], orc.edm(pts))
 
 
+@pytest.mark.parametrize("rho", [128, 256])
 @pytest.mark.parametrize("dim", [1, 2, 4])
-def test_edm_dims_and_stride(orc, dim):
-    n = 777
+def test_edm_dims_and_stride(orc, dim, rho):
+    n = 777 if rho == 128 else 1601
     pts = inputs.points(n, dim, 7)
-    m = tri.tri_map_init(n, 128)
+    m = tri.tri_map_init(n, rho)
     out = torch.empty((m.out_cells,), dtype=torch.float32, device="cuda")
     wide = torch.zeros((n, 6), dtype=torch.float32)
     wide[:, :dim] = torch.from_numpy(pts)

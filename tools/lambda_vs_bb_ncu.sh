@@ -15,8 +15,9 @@ for s in lambda bb; do
   run collide1d_$s collide1d_kernel collide1d --strategy $s
   run ca_multi_$s ca_multi_kernel ca_steps --rho 224 --k 8 --strategy $s
   run ca_step_$s ca_multi_kernel ca --rho 128 --strategy $s
+  run ca_packed_$s ca_packed_kernel ca_run --rho 240 --k 8 --strategy $s
   run triplet_$s triplet32_kernel triplet --rho 32 --strategy $s
 done
-run collide_tc_lambda collide_tc_kernel collide --rho 1024 --strategy tc
-run collide_tc_bb collide_tc_kernel collide --rho 1024 --strategy bb_tc
+run collide_tc_lambda collide_tc_kernel collide --rho 768 --strategy tc
+run collide_tc_bb collide_tc_kernel collide --rho 768 --strategy bb_tc
 ls gpurun_out/lvb

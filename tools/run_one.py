@@ -1,6 +1,6 @@
 """Run one hot-path kernel a few times (for ncu captures and quick sweeps).
 
-python tools/run_one.py edm|dummy|collide|collide1d|ca|ca_steps|triplet [--rho R] [--strategy S] [--reps K] [--n N]
+python tools/run_one.py edm|dummy|collide|collide1d|ca|ca_steps|ca_run|triplet [--rho R] [--strategy S] [--reps K] [--n N]
 Prints per-launch CUDA-event times (ms).  Product path only (no oracle)."""
 import argparse
 import os
@@ -52,6 +52,13 @@ def main():
         x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
         y = torch.empty_like(x)
         fn = lambda: tri.tri_ca_steps(m, a.strategy, a.k, x, y)
+    elif w == "ca_run":                       # tri_ca_run: --k generations on the bit-packed state
+        n = a.n or 32768
+        m = tri.tri_map_init(n, a.rho or 240)
+        x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
+        y = torch.empty_like(x)
+        ws = torch.empty(tri.tri_ca_run_workspace_size(m), dtype=torch.uint8, device="cuda")
+        fn = lambda: tri.tri_ca_run(m, a.strategy, a.k, x, y, ws)
     elif w == "collide1d":
         n = a.n or 200000
         m = tri.tri_map_init(n, a.rho or 256)
