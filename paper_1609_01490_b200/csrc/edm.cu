@@ -17,12 +17,16 @@
 // data).  Interior tiles (bj + 1 < bi: every line stays inside its row) take the fast
 // path edm_tile_interior_line: column points staged once per tile in shared memory as
 // four rotated SoA copies (one aligned LDS.128 per coordinate per lane at any phase),
-// row points as float4s, rows i and i + 64 (same phase) walked as a pair so one set of
-// column loads serves 8 cells per lane, two cells per FADD2/FMUL2/FFMA2; 4 CTAs per SM.
-// Round 2 measured 1.39 -> 1.28 ms per step in the bench's sustained loop (n = 65536,
-// 3-D) and 1.55 -> 1.27 ms for 4 features; single rows with shared-memory columns and
-// scalar math were slower than the chunk form (1.55 vs 1.47 ms: more instructions
-// under the board's power cap), 5 CTAs per SM within noise of 4, 3 / 2 CTAs slower.
+// row points as float4s, the tile's rows walked as 32 same-phase quads {x, 63-x, 64+x,
+// 127-x} so one set of column loads serves 16 cells per lane, two cells per
+// FADD2/FMUL2/FFMA2; 4 CTAs per SM.  Round 2 measured 1.39 -> 1.28 ms per step in the
+// bench's sustained loop (n = 65536, 3-D) and 1.55 -> 1.27 ms for 4 features.  In that loop
+// the board sits at its 1 kW power cap (SM clock ~1.6 GHz, sw_power_cap): the stores alone
+// cost 0.84 J per launch (= torch fill_), the arithmetic ~0.3 J more
+// (profiles/r02_edm_power.txt), so instruction count, not the write pattern, now sets the
+// sustained rate; isolated launches take 1.18 ms (7.3 TB/s).  Single rows with scalar math
+// were slower than the chunk form; row pairs (i, i + 64) equal to quads; 5 CTAs per SM
+// within noise of 4, 3 / 2 CTAs slower; rho = 256 tiles (1 KB row segments) slower.
 //
 // Other tile edges: interior tiles walk ROWS rows per warp, lane k owning chunk k
 // (rho = 32 CW, so each warp store is one contiguous 512 B / 1 KB run); the row's
@@ -173,68 +177,57 @@ template <int RHO> struct OwnW { static constexpr int OW = (RHO == 128 && TRI_ED
 constexpr int kLineCols = 160;        // staged columns c0 + t (t < 160) per rotation: lanes reach 4 (31 + 7) + 3
 template <int DIM> struct LineSmem { static constexpr int FLOATS = 4 * DIM * kLineCols + 4 * 128; };
 
+// One row quad of a line-owned interior tile: tile rows {x, 63 - x, 64 + x, 127 - x} share
+// the line phase (T(r0 + y) = T(r0) + r0 y + T(y) with r0 = 0 mod 128, and T(y) mod 32 is
+// the same on exactly these four y < 128), so one set of column loads serves 16 cells per
+// lane.  FULL: all four rows inside the domain, else bit g of vmask says row g is.
+template <int DIM, bool FULL>
+__device__ __forceinline__ void edm_line_quad(const float *rl, const float4 *rowp, int x, float *const (&pr)[4],
+                                              uint32_t s32, int vmask) {
+    const int delta = (int)((0u - s32) & 31u);
+    const float *src = rl + (delta & 3) * DIM * kLineCols + (delta & ~3);
+    ulonglong2 w[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) w[d] = *reinterpret_cast<const ulonglong2 *>(src + d * kLineCols);
+    const int rows[4] = {x, 63 - x, 64 + x, 127 - x};
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        if (!FULL && !((vmask >> g) & 1)) continue;
+        const float4 pq = rowp[rows[g]];
+        const float pv[4] = {pq.x, pq.y, pq.z, pq.w};
+        unsigned long long a01 = 0, a23 = 0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+            unsigned long long e01, e23, pp;
+            asm("mov.b64 %0, {%1, %1};" : "=l"(pp) : "f"(pv[d]));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e01) : "l"(pp), "l"(w[d].x));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e23) : "l"(pp), "l"(w[d].y));
+            if (d == 0) {
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(a01) : "l"(e01));
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(a23) : "l"(e23));
+            } else {
+                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(a01) : "l"(e01));
+                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(a23) : "l"(e23));
+            }
+        }
+        float v[4];
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(a01));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(a23));
+        st_cs_v4(pr[g] + delta, sqrt_approx(v[0]), sqrt_approx(v[1]), sqrt_approx(v[2]), sqrt_approx(v[3]));
+    }
+}
+
 // Interior tile, line ownership (rho = 128).  The row's line phase delta = (-T(i)) mod 32 =
 // 4a + b is warp-uniform; lane k writes cells delta + 4k .. + 3 of the segment, i.e. columns
 // c0 + 4(k + a) + b + e.  The tile's 163 column points are staged in shared memory as four
 // rotated SoA copies rot[b][d][t] = point (c0 + t + b), so every lane reads its 4 columns of
 // one coordinate with one aligned LDS.128 (a warp reads 512 contiguous bytes: 4 wavefronts),
-// and the tile's 128 row points as float4s (one broadcast LDS.128 per row).  Rows i and
-// i + 64 have the same phase (T(i + 64) - T(i) = 64 i + 2080 = 0 mod 32), so a warp walks
-// row PAIRS (i, i + 64): one set of column loads serves 8 cells per lane.
-// One row pair (i, i + 64) of a line-owned interior tile: lane's chunk at the row's phase.
-template <int DIM, bool SECOND>
-__device__ __forceinline__ void edm_line_pair(const float *rl, const float4 *rp, float *&pa_row, float *&pb_row,
-                                              uint32_t &s32, uint32_t &inc) {
-    const int delta = (int)((0u - s32) & 31u);
-    const float *src = rl + (delta & 3) * DIM * kLineCols + (delta & ~3);
-    const float4 pa = rp[0], pb = rp[64];
-    const float pav[4] = {pa.x, pa.y, pa.z, pa.w}, pbv[4] = {pb.x, pb.y, pb.z, pb.w};
-    unsigned long long a01 = 0, a23 = 0, b01 = 0, b23 = 0;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-        const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(src + d * kLineCols);
-        unsigned long long e01, e23, f01, f23, pp, qq;
-        asm("mov.b64 %0, {%1, %1};" : "=l"(pp) : "f"(pav[d]));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e01) : "l"(pp), "l"(w.x));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e23) : "l"(pp), "l"(w.y));
-        if (d == 0) {
-            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(a01) : "l"(e01));
-            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(a23) : "l"(e23));
-        } else {
-            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(a01) : "l"(e01));
-            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(a23) : "l"(e23));
-        }
-        if constexpr (SECOND) {
-            asm("mov.b64 %0, {%1, %1};" : "=l"(qq) : "f"(pbv[d]));
-            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f01) : "l"(qq), "l"(w.x));
-            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f23) : "l"(qq), "l"(w.y));
-            if (d == 0) {
-                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(b01) : "l"(f01));
-                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(b23) : "l"(f23));
-            } else {
-                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(b01) : "l"(f01));
-                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(b23) : "l"(f23));
-            }
-        }
-    }
-    float v[8];
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(a01));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(a23));
-    st_cs_v4(pa_row + delta, sqrt_approx(v[0]), sqrt_approx(v[1]), sqrt_approx(v[2]), sqrt_approx(v[3]));
-    if constexpr (SECOND) {
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[4]), "=f"(v[5]) : "l"(b01));
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[6]), "=f"(v[7]) : "l"(b23));
-        st_cs_v4(pb_row + delta, sqrt_approx(v[4]), sqrt_approx(v[5]), sqrt_approx(v[6]), sqrt_approx(v[7]));
-    }
-    pa_row += inc;                                            // T(i + 1) = T(i) + i + 1
-    pb_row += inc + 64u;
-    s32 += inc;
-    ++inc;
-}
-
+// and the tile's 128 row points as float4s (one broadcast LDS.128 per row).  The 128 rows
+// fall into 32 classes of four with the same phase (edm_line_quad), so a warp walks four
+// row QUADS: one set of column loads serves 16 cells per lane.
 template <int DIM, bool VEC4 = false>
 __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t r0, int64_t c0, float *rot) {
-    constexpr int RHO = 128, PAIRS = RHO / 2 / kWarps;        // 8 row pairs per warp
+    constexpr int RHO = 128;
     float4 *rowp = reinterpret_cast<float4 *>(rot + 4 * DIM * kLineCols);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __syncthreads();                                          // the previous tile's readers are done
@@ -262,27 +255,32 @@ __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t
         }
     }
     __syncthreads();
-    const int64_t i0 = r0 + (int64_t)warp * PAIRS;            // first row of the pair walk
-    if (i0 >= a.n) return;
-    const uint64_t s0 = tri::T2((uint64_t)i0) + (uint64_t)c0 - a.out_offset;   // local start of row i0
-    float *pa_row = a.out + s0 + 4 * lane;                    // row i, lane's chunk at phase 0
-    float *pb_row = pa_row + (64u * (uint64_t)i0 + 2080u);    // row i + 64 (T(i + 64) - T(i))
-    uint32_t s32 = (uint32_t)s0;                              // low bits of the row start (phase)
-    const int na = (int)((a.n - i0) < PAIRS ? (a.n - i0) : PAIRS);              // rows i < n
-    const int nb = (int)((a.n - i0 - 64) < PAIRS ? ((a.n - i0 - 64) > 0 ? (a.n - i0 - 64) : 0) : PAIRS);
-    const float *rl = rot + 4 * lane;
-    const float4 *rp = rowp + warp * PAIRS;
-    uint32_t inc = (uint32_t)i0 + 1u;                         // T(i + 1) - T(i)
-    if (nb == PAIRS) {                                        // every row pair inside (all but the last tile row)
+    // warp w takes x = 4w .. 4w + 3: rows {x, 63 - x, 64 + x, 127 - x}, all 128 rows over 8 warps
+    const int x0 = 4 * warp;
+    const int64_t rr0[4] = {r0 + x0, r0 + 63 - x0, r0 + 64 + x0, r0 + 127 - x0};
+    float *pr[4];
 #pragma unroll
-        for (int t = 0; t < PAIRS; ++t)
-            edm_line_pair<DIM, true>(rl, rp + t, pa_row, pb_row, s32, inc);
-    } else {
-#pragma unroll 1
-        for (int t = 0; t < na; ++t) {
-            if (t < nb) edm_line_pair<DIM, true>(rl, rp + t, pa_row, pb_row, s32, inc);
-            else edm_line_pair<DIM, false>(rl, rp + t, pa_row, pb_row, s32, inc);
+    for (int g = 0; g < 4; ++g)
+        pr[g] = a.out + (tri::T2((uint64_t)rr0[g]) + (uint64_t)c0 - a.out_offset) + 4 * lane;
+    uint32_t s32 = (uint32_t)(tri::T2((uint64_t)rr0[0]) + (uint64_t)c0 - a.out_offset);   // phase bits
+    const float *rl = rot + 4 * lane;
+    const bool full = r0 + 127 < a.n;
+    const uint32_t u0 = (uint32_t)r0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int x = x0 + t;
+        if (full) {
+            edm_line_quad<DIM, true>(rl, rowp, x, pr, s32, 15);
+        } else {
+            const int vmask = (r0 + x < a.n) | ((r0 + 63 - x < a.n) << 1) | ((r0 + 64 + x < a.n) << 2) |
+                              ((r0 + 127 - x < a.n) << 3);
+            if (vmask) edm_line_quad<DIM, false>(rl, rowp, x, pr, s32, vmask);
         }
+        pr[0] += u0 + (uint32_t)x + 1u;                   // T(i + 1) - T(i) = i + 1
+        pr[1] -= u0 + 63u - (uint32_t)x;                  // T(i - 1) - T(i) = -i
+        pr[2] += u0 + 65u + (uint32_t)x;
+        pr[3] -= u0 + 127u - (uint32_t)x;
+        s32 += u0 + (uint32_t)x + 1u;
     }
 }
 
