@@ -68,7 +68,8 @@ def ncu_traffic(name):
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw.instant,"
+              "power.limit")
 
     def __init__(self, dev_index):
         self.dev = dev_index
@@ -101,7 +102,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, mx, pw, reasons = [], [], [], set()
+        sm, mx, pw, pwi, lim, reasons = [], [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -114,8 +115,15 @@ class ClockSampler:
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
+            try:                                   # instantaneous board power (power.draw is a 1-s average)
+                pwi.append(float(f[9])); lim.append(float(f[10]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "power_w_max": max(pw) if pw else None, "reasons": sorted(reasons), "samples": len(sm)}
+                "power_w_max": max(pwi) if pwi else (max(pw) if pw else None),
+                "power_w_median": statistics.median(pwi) if pwi else None,
+                "power_avg1s_w_max": max(pw) if pw else None, "power_limit_w": max(lim) if lim else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ----------------------------------------------------------------------------- timing helpers

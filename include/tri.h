@@ -144,6 +144,15 @@ tri_status tri_map_eval(uint64_t omega0, uint64_t count, uint32_t *d_ij,
 tri_status tri_map_eval_variant(int32_t variant, uint64_t omega0, uint64_t count,
                                 unsigned long long *d_fail, unsigned long long *d_first, void *stream);
 
+/* Rows of a square-root variant (TRI_SQRT_X / _N / _R), uncorrected: d_rows[t] (u32,
+ * rows_bytes >= 4 count, 4-byte aligned) = the variant's row i at omega0 + t, i.e.
+ * floor(sqrt_variant(1/4 + 2 omega) - 1/2) in fp32.  lambda_R's row depends
+ * on the hardware rsqrtf, which is specified only to 2 ulp: tests check these rows
+ * against the oracle's reachable-row interval (reading Q5c).
+ * EINVAL: bad variant / pointer / capacity; ERANGE: omega0 + count > 2^40. */
+tri_status tri_map_rows_variant(int32_t variant, uint64_t omega0, uint64_t count, uint32_t *d_rows,
+                                size_t rows_bytes, void *stream);
+
 /* Dummy kernel: each useful thread maps itself to (i,j).
  *   FIXED  : writes i + j to d_out[0] (u32; racy by design)
  *   PACKED : d_out[T(i)+j - out_offset] = (i<<16)|j as u32 when n <= 65536, else

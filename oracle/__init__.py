@@ -70,6 +70,8 @@ def lib():
         L.orc_set_threads.restype = None
         L.orc_variant_scan.argtypes = [i32, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]
         L.orc_collide1d.argtypes = [i64, vp, i64, i64, ctypes.POINTER(u64)]
+        L.orc_variant_r_rows.argtypes = [u64, u64, ctypes.c_double, vp, vp]
+        L.orc_variant_r_scan.argtypes = [u64, u64, ctypes.c_double] + [ctypes.POINTER(u64)] * 4
         _lib = L
     return _lib
 
@@ -146,6 +148,28 @@ def variant_scan(variant: int, w0: int, count: int):
     f, first = u64(), u64()
     _check(lib().orc_variant_scan(variant, w0, count, ctypes.byref(f), ctypes.byref(first)))
     return f.value, (None if first.value == 2**64 - 1 else first.value)
+
+
+RSQRTF_REL = 2.0 ** -22        # rsqrtf: 2 ulp (CUDA Math API) -- DESIGN.md reading Q5c
+
+
+def variant_r_rows(w0: int, count: int, rel: float = RSQRTF_REL):
+    """lambda_R within rsqrtf's error bound: per omega in [w0, w0+count) the
+    lowest and highest row any fp32 r with |r sqrt(x) - 1| <= rel can give."""
+    lo, hi = np.zeros(count, np.uint32), np.zeros(count, np.uint32)
+    _check(lib().orc_variant_r_rows(w0, count, rel, _ptr(lo), _ptr(hi)))
+    return lo, hi
+
+
+def variant_r_scan(w0: int, count: int, rel: float = RSQRTF_REL):
+    """(n surely wrong, first surely wrong, n maybe wrong, first maybe wrong) for lambda_R on
+    [w0, w0+count): surely = the exact row is reachable by no admissible rsqrtf, maybe = by
+    not every one.  first = None when there is none."""
+    a, b, c, d = u64(), u64(), u64(), u64()
+    _check(lib().orc_variant_r_scan(w0, count, rel, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                    ctypes.byref(d)))
+    nn = lambda v: None if v == 2**64 - 1 else v
+    return a.value, nn(b.value), c.value, nn(d.value)
 
 
 # --- dummy ----------------------------------------------------------------

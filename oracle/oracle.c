@@ -460,7 +460,8 @@ int orc_triplet_total(int64_t n, const float *pts, double nu, double *total)
 /*     operation order is kept (it decides the first failing omega,            */
 /*     tests/golden/sqrt_variants.txt; reading Q5b).                 */
 /* every operation IEEE fp32 round-to-nearest in this order (no contraction).  */
-/* lambda_R (hardware rsqrt) has no CPU definition: parity unpinned.           */
+/* lambda_R (hardware rsqrt) has no bit-exact CPU definition: see            */
+/* orc_variant_r_* below (its result within rsqrtf's documented error bound).  */
 /* The variant is correct at w iff T(i) <= w < T(i+1) (Eq. 3).      */
 /* Returns the number of failures in [w0, w0+count) and the first failing w    */
 /* (UINT64_MAX if none).                                                       */
@@ -503,6 +504,67 @@ int orc_variant_scan(int32_t variant, uint64_t w0, uint64_t count, uint64_t *fai
     }
     *fails = nf;
     *first = fw;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* lambda_R: s = x * rsqrtf(x) + 1e-4, i = floor(s - 1/2), with    */
+/* x = 1/4 + 2 w, every operation IEEE fp32 round-to-nearest.  rsqrtf itself    */
+/* is specified only to within 2 ulp (CUDA Math API; the PTX rsqrt.approx.f32  */
+/* bound 2^-22.9 is tighter), so lambda_R's row is not a single number: this    */
+/* computes the rows reachable by EVERY fp32 r with |r sqrt(x) - 1| <= rel      */
+/* (r bracketed outward to fp32 from the fp64 1/sqrt(x)).  The row is monotone  */
+/* in r, so the reachable rows lie in [row(r_lo), row(r_hi)].  A w is SURELY    */
+/* wrong when the exact row (Eq. 3) is outside that interval, MAYBE wrong when  */
+/* the interval holds it and another row.  DESIGN.md reading Q5c.              */
+/* ------------------------------------------------------------------------ */
+static uint32_t variant_r_row(float x, float r)
+{
+    float xr = x * r;
+    float s = xr + 1e-4f;
+    float f = floorf(s - 0.5f);
+    return f > 0.0f ? (uint32_t)f : 0u;
+}
+
+static void variant_r_bracket(uint64_t w, double rel, uint32_t *ilo, uint32_t *ihi)
+{
+    float x = 0.25f + 2.0f * (float)w;
+    double q = 1.0 / sqrt((double)x);
+    double qlo = q * (1.0 - rel) * (1.0 - 1e-15), qhi = q * (1.0 + rel) * (1.0 + 1e-15);
+    float rlo = (float)qlo, rhi = (float)qhi;                  /* round outward to fp32 */
+    if ((double)rlo > qlo) rlo = nextafterf(rlo, 0.0f);
+    if ((double)rhi < qhi) rhi = nextafterf(rhi, INFINITY);
+    *ilo = variant_r_row(x, rlo);
+    *ihi = variant_r_row(x, rhi);
+}
+
+int orc_variant_r_rows(uint64_t w0, uint64_t count, double rel, uint32_t *ilo, uint32_t *ihi)
+{
+    if (!(rel >= 0.0 && rel < 1e-3)) return ORC_EINVAL;
+    for (uint64_t t = 0; t < count; ++t) variant_r_bracket(w0 + t, rel, ilo + t, ihi + t);
+    return ORC_OK;
+}
+
+int orc_variant_r_scan(uint64_t w0, uint64_t count, double rel, uint64_t *n_sure, uint64_t *first_sure,
+                       uint64_t *n_maybe, uint64_t *first_maybe)
+{
+    if (!(rel >= 0.0 && rel < 1e-3)) return ORC_EINVAL;
+    uint64_t ns = 0, fs = UINT64_MAX, nm = 0, fm = UINT64_MAX;
+    #pragma omp parallel for schedule(static) reduction(+:ns,nm) reduction(min:fs,fm)
+    for (uint64_t t = 0; t < count; ++t) {
+        uint64_t w = w0 + t;
+        uint32_t lo, hi;
+        variant_r_bracket(w, rel, &lo, &hi);
+        uint64_t i = 0;                                            /* exact row by bisection on Eq. 3 */
+        uint64_t a = 0, b = 1u << 21;
+        while (a < b) { uint64_t mid = (a + b + 1) / 2; if (T2(mid) <= w) a = mid; else b = mid - 1; }
+        i = a;
+        int sure_ok = lo == hi && lo == i;
+        int sure_bad = i < lo || i > hi;
+        if (!sure_ok) { nm += 1; if (w < fm) fm = w; }
+        if (sure_bad) { ns += 1; if (w < fs) fs = w; }
+    }
+    *n_sure = ns; *first_sure = fs; *n_maybe = nm; *first_maybe = fm;
     return ORC_OK;
 }
 

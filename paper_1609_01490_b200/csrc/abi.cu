@@ -148,6 +148,15 @@ tri_status tri_map_eval_variant(int32_t variant, uint64_t omega0, uint64_t count
     return launch_variant_scan(variant, omega0, count, d_fail, d_first, (cudaStream_t)stream);
 }
 
+tri_status tri_map_rows_variant(int32_t variant, uint64_t omega0, uint64_t count, uint32_t *d_rows,
+                                size_t rows_bytes, void *stream) {
+    g_launches = 0;
+    if (!d_rows || (((uintptr_t)d_rows) & 3u) || variant < TRI_SQRT_X || variant > TRI_SQRT_R) return TRI_EINVAL;
+    if (omega0 > TRI_OMEGA_MAX || count > TRI_OMEGA_MAX - omega0) return TRI_ERANGE;
+    if (rows_bytes / 4u < count) return TRI_EINVAL;
+    return launch_variant_rows(variant, omega0, count, d_rows, (cudaStream_t)stream);
+}
+
 static bool bad_strategy(int32_t s) { return s != TRI_LAMBDA && s != TRI_BB && s != TRI_LAMBDA_PERSIST; }
 
 static bool bad_map(const tri_map_t *m) {

@@ -82,6 +82,16 @@ __global__ void __launch_bounds__(256) variant_scan_kernel(int variant, uint64_t
     }
 }
 
+// Rows of an uncorrected square-root variant: rows[t] = the variant's i at omega0 + t.
+__global__ void __launch_bounds__(256) variant_rows_kernel(int variant, uint64_t w0, uint64_t count, uint32_t *rows) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+        uint32_t vi, vj;
+        tri::lambda_variant(w0 + t, variant, vi, vj);
+        rows[t] = vi;
+    }
+}
+
 // ---- succinct layer table: S[k] = T3(k), G[g] = max{k : T3(k) <= g << shift}
 struct TetLut {
     const uint64_t *S;
@@ -175,6 +185,13 @@ tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigne
     if (cudaMemsetAsync(d_first, 0xff, sizeof(unsigned long long), st) != cudaSuccess) return TRI_ECUDA;
     if (count == 0) return TRI_OK;
     variant_scan_kernel<<<eval_grid(count), 256, 0, st>>>(variant, w0, count, d_fail, d_first);
+    note_launches(1);
+    return cuda_status();
+}
+
+tri_status launch_variant_rows(int variant, uint64_t w0, uint64_t count, uint32_t *d_rows, cudaStream_t st) {
+    if (count == 0) return TRI_OK;
+    variant_rows_kernel<<<eval_grid(count), 256, 0, st>>>(variant, w0, count, d_rows);
     note_launches(1);
     return cuda_status();
 }

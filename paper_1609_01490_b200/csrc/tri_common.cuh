@@ -291,6 +291,7 @@ tri_status launch_tet_map_eval_lut(uint64_t w0, uint64_t count, uint32_t kmax, i
                                    uint32_t *d_ijk, unsigned long long *d_fail, cudaStream_t st);
 tri_status launch_variant_scan(int variant, uint64_t w0, uint64_t count, unsigned long long *d_fail,
                                unsigned long long *d_first, cudaStream_t st);
+tri_status launch_variant_rows(int variant, uint64_t w0, uint64_t count, uint32_t *d_rows, cudaStream_t st);
 tri_status launch_dummy_rb(const tri_map_t &m, int mode, void *d_out, cudaStream_t st);
 tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph, unsigned long long *count,
                              void *ws, cudaStream_t st);

@@ -68,6 +68,7 @@ SIGNATURES = {
     "tri_collide1d": ([ctypes.POINTER(TriMap), c_i32, c_vp, ctypes.c_size_t, c_vp, ctypes.c_size_t, c_vp], c_i32),
     "tri_map_eval": ([c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
     "tri_map_eval_variant": ([c_i32, c_u64, c_u64, c_vp, c_vp, c_vp], c_i32),
+    "tri_map_rows_variant": ([c_i32, c_u64, c_u64, c_vp, c_sz, c_vp], c_i32),
     "tri_dummy": ([ctypes.POINTER(TriMap), c_i32, c_i32, c_vp, ctypes.c_size_t, c_vp], c_i32),
     "tri_edm": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_i32, c_i64, c_sz, c_vp, c_sz, c_vp], c_i32),
     "tri_edm_host": ([ctypes.POINTER(TriMap), c_i32, c_vp, c_i32, c_i64, c_sz, c_vp, c_sz, c_vp, c_sz,
@@ -189,6 +190,13 @@ def tri_collide1d(m: TriMap, strategy, intervals, count, stream=None):
 
 def tri_map_eval(omega0, count, d_ij, d_fail, stream=None):
     _ok(lib().tri_map_eval(omega0, count, _ptr(d_ij), _ptr(d_fail), _stream(stream)), "tri_map_eval")
+
+
+def tri_map_rows_variant(variant, omega0, count, d_rows, stream=None):
+    """d_rows: int32/uint32 CUDA tensor >= count: the uncorrected variant's row per omega."""
+    _need(d_rows.is_cuda and d_rows.element_size() == 4, "tri_map_rows_variant: d_rows must be 4-byte CUDA")
+    _ok(lib().tri_map_rows_variant(variant, omega0, count, _ptr(d_rows), _nbytes(d_rows), _stream(stream)),
+        "tri_map_rows_variant")
 
 
 def tri_map_eval_variant(variant, omega0, count, d_fail, d_first, stream=None):

@@ -328,3 +328,16 @@ def test_ca_run_validation(L):
     assert run(m, st=tri.TRI_LAMBDA_CLC) == tri.TRI_EINVAL
     assert run(tri.tri_map_init(n, 224)) == tri.TRI_EINVAL                 # rho 240 only
     assert run(tri.tri_map_init(n, 240, 1, 0, 2, 1)) == tri.TRI_EINVAL     # one rank only
+
+
+def test_map_rows_variant_validation(L):
+    """tri_map_rows_variant: a bad variant, a NULL / misaligned pointer or a short capacity
+    is EINVAL, an omega range past 2^40 ERANGE -- synchronously, before any launch."""
+    import ctypes
+    p = ctypes.c_void_p(1 << 20)
+    assert L.tri_map_rows_variant(0, 0, 10, p, 40, None) == tri.TRI_EINVAL          # not a variant
+    assert L.tri_map_rows_variant(4, 0, 10, p, 40, None) == tri.TRI_EINVAL
+    assert L.tri_map_rows_variant(3, 0, 10, None, 40, None) == tri.TRI_EINVAL
+    assert L.tri_map_rows_variant(3, 0, 10, ctypes.c_void_p((1 << 20) + 2), 40, None) == tri.TRI_EINVAL
+    assert L.tri_map_rows_variant(3, 0, 10, p, 39, None) == tri.TRI_EINVAL           # 10 rows need 40 B
+    assert L.tri_map_rows_variant(3, 1 << 40, 1, p, 4, None) == tri.TRI_ERANGE

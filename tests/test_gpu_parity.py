@@ -109,9 +109,46 @@ def test_sqrt_variant_scan_matches_oracle(orc, variant, count):
     assert first.item() == g[variant]           # SURVEY.md:38-40
 
 
+def test_lambda_r_rows_within_rsqrtf_bound(orc):
+    """lambda_R depends on the hardware rsqrtf, specified to 2 ulp (reading Q5c):
+    every GPU row for omega < 2^23 lies in the oracle's reachable-row interval, and the GPU
+    scan over [0, 2^24) fails on at least every surely-wrong and at most every maybe-wrong
+    omega, no earlier than the first maybe-wrong one."""
+    cnt = 1 << 23
+    rows = torch.empty(cnt, dtype=torch.int32, device="cuda")
+    tri.tri_map_rows_variant(tri.TRI_SQRT_R, 0, cnt, rows)
+    sync()
+    got = rows.cpu().numpy().astype(np.int64)
+    lo, hi = orc.variant_r_rows(0, cnt)
+    assert np.all(lo.astype(np.int64) <= got) and np.all(got <= hi.astype(np.int64))
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tri.tri_map_eval_variant(tri.TRI_SQRT_R, 0, 1 << 24, fail, first)
+    sync()
+    ns, fs, nm, fm = orc.variant_r_scan(0, 1 << 24)
+    assert ns <= fail.item() <= nm
+    if fail.item():
+        assert first.item() >= fm and (fs is None or first.item() <= fs)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_variant_rows_match_scan(orc, variant):
+    """tri_map_rows_variant's lambda_X / lambda_N rows are the IEEE-deterministic ones: judged
+    by Eq. 3 they fail exactly where the oracle scan says (count and first omega)."""
+    cnt = 1 << 21
+    rows = torch.empty(cnt, dtype=torch.int32, device="cuda")
+    tri.tri_map_rows_variant(variant, 0, cnt, rows)
+    sync()
+    i = rows.cpu().numpy().astype(np.int64)
+    w = np.arange(cnt, dtype=np.int64)
+    bad = ~((i * (i + 1) // 2 <= w) & (w < (i + 1) * (i + 2) // 2))
+    nf, fw = orc.variant_scan(variant, 0, cnt)
+    assert int(bad.sum()) == nf and (int(w[np.argmax(bad)]) if bad.any() else None) == fw
+
+
 def test_sqrt_variant_r_runs_and_dummy_variants():
-    """lambda_R depends on MUFU.RSQ rounding (parity unpinned): the scan runs; inside
-    the first-failure bound the variant dummy kernels give the exact digest."""
+    """The lambda_R scan runs; inside the first-failure bound the variant dummy kernels
+    give the exact digest."""
     fail = torch.zeros(1, dtype=torch.int64, device="cuda")
     first = torch.zeros(1, dtype=torch.int64, device="cuda")
     tri.tri_map_eval_variant(tri.TRI_SQRT_R, 0, 1 << 24, fail, first)

@@ -549,3 +549,62 @@ def test_sqrt_variant_x_exact_rational_boundaries():
             if w <= g:
                 r = _exact_row_x(w)
                 assert (T(r) <= w < T(r + 1)) == (w < g), (i, w, r)
+
+
+# ------------------------------------------------ lambda_R within rsqrtf's error bound (Q5c)
+def _np_lambda_r_rows(w):
+    """Independent numpy restatement of lambda_R with a CORRECTLY ROUNDED
+    reciprocal square root (fp64 1/sqrt rounded once to fp32: within 0.5 ulp, so inside
+    any 2-ulp rsqrtf bound): x = 1/4 + 2w, s = x r + 1e-4, i = floor(s - 1/2), fp32."""
+    f32 = np.float32
+    x = (f32(0.25) + f32(2.0) * w.astype(np.float32)).astype(np.float32)
+    r = (1.0 / np.sqrt(x.astype(np.float64))).astype(np.float32)
+    s = ((x * r).astype(np.float32) + f32(1e-4)).astype(np.float32)
+    return np.maximum(np.floor((s - f32(0.5)).astype(np.float32)), 0).astype(np.int64)
+
+
+def _exact_rows(w):
+    from math import isqrt
+    return np.array([(isqrt(8 * int(v) + 1) - 1) // 2 for v in w], np.int64)
+
+
+def test_lambda_r_bracket_holds_a_correctly_rounded_rsqrt(orc):
+    """Every omega < 3,000,000: the numpy lambda_R row (an admissible rsqrtf) lies in the
+    oracle's reachable-row interval, at the 2-ulp bound and at the PTX 2^-22.9 bound."""
+    for rel in (orc.RSQRTF_REL, 2.0 ** -22.9):
+        for a in range(0, 3_000_000, 1 << 20):
+            cnt = min(3_000_000, a + (1 << 20)) - a
+            w = np.arange(a, a + cnt, dtype=np.int64)
+            lo, hi = orc.variant_r_rows(a, cnt, rel)
+            r = _np_lambda_r_rows(w)
+            assert np.all(lo.astype(np.int64) <= r) and np.all(r <= hi.astype(np.int64))
+            assert np.all(hi.astype(np.int64) - lo.astype(np.int64) <= 1)   # 2 ulp moves a row by <= 1
+
+
+def test_lambda_r_bracket_exact_where_the_bound_cannot_matter(orc):
+    """Small omega: the eps = 1e-4 slack exceeds any 2-ulp error of x r, so every admissible
+    rsqrtf gives the exact row (Eq. 3); checked against the integer closed form."""
+    w = np.arange(0, 20_000, dtype=np.int64)
+    lo, hi = orc.variant_r_rows(0, len(w))
+    ex = _exact_rows(w)
+    assert np.array_equal(lo.astype(np.int64), ex) and np.array_equal(hi.astype(np.int64), ex)
+
+
+def test_lambda_r_scan_consistent_with_rows(orc):
+    """The scan's surely / maybe wrong counts equal those of the per-omega intervals judged
+    with the integer closed form (a different exact-row route than the scan's bisection),
+    and the numpy lambda_R's failures sit inside the maybe set."""
+    a, cnt = 2_000_000, 1 << 20
+    w = np.arange(a, a + cnt, dtype=np.int64)
+    lo, hi = orc.variant_r_rows(a, cnt)
+    lo, hi = lo.astype(np.int64), hi.astype(np.int64)
+    ex = np.floor((np.sqrt(8.0 * w + 1.0) - 1.0) / 2.0).astype(np.int64)   # exact: 8w+1 < 2^53
+    ok = (ex * (ex + 1) // 2 <= w) & (w < (ex + 1) * (ex + 2) // 2)
+    assert ok.all()
+    sure_bad = (ex < lo) | (ex > hi)
+    maybe_bad = ~((lo == hi) & (lo == ex))
+    ns, fs, nm, fm = orc.variant_r_scan(a, cnt)
+    assert (ns, nm) == (int(sure_bad.sum()), int(maybe_bad.sum()))
+    assert fm == (int(w[np.argmax(maybe_bad)]) if maybe_bad.any() else None)
+    r = _np_lambda_r_rows(w)
+    assert not np.any((r != ex) & ~maybe_bad)
