@@ -38,13 +38,13 @@
 // ONE contiguous rho x 32-byte run each, staged into shared memory by two 1-D bulk copies
 // (cp.async.bulk, the TMA engine) completing on an mbarrier.
 //
-// CTA = 128 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB grid,
+// CTA = 256 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB grid,
 // P:411-418), 128 TMEM columns.  Per 128 x 128 block one MMA (issued by one thread)
-// commits to an mbarrier; thread t = accumulator lane t = row t of the block loads its 128
-// columns (4 x tcgen05.ld.32x32b.x16.pack::16b: two F16 values per register, 64
-// registers), the CTA hands the accumulator back (one barrier) and thread 0 issues the
-// next block's MMA while every thread ORs its 64 registers (32 three-input LOP3s: a
-// quarter of an ALU op per pair) and tests bits 15 and 31.  A flagged (row, 32-column)
+// commits to an mbarrier; threads t and t + 128 = accumulator lane t & 127 = row t & 127 of
+// the block load one half of its 128 columns each (2 x tcgen05.ld.32x32b.x16.pack::16b: two
+// F16 values per register, 32 registers), the CTA hands the accumulator back (one barrier)
+// and thread 0 issues the next block's MMA while every thread ORs its 32 registers (16
+// three-input LOP3s: a quarter of an ALU op per pair) and tests bits 15 and 31.  A flagged (row, 32-column)
 // group recounts only its negative columns with the exact predicate.  Diagonal tiles skip
 // the blocks above the diagonal and recount j < i only.  (Round 2 history in DESIGN.md:
 // the single-pass TF32 filter with F32 accumulators this replaces, persistent
@@ -54,7 +54,18 @@
 
 namespace {
 
-constexpr int kThreads = 128, kCols = 128;
+constexpr int kThreads = 128, kCols = 128;            // probes: one thread per accumulator lane
+#ifndef TRI_TC_HALVES
+#define TRI_TC_HALVES 2
+#endif
+// tile kernel: warps w and w + 4 (w < 4) read TMEM lane quarter w; with TRI_TC_HALVES = 2 each
+// takes half of the 128 accumulator columns (8 warps per CTA, half the sign-test work each)
+constexpr int kHalves = TRI_TC_HALVES, kTileThreads = 128 * kHalves, kColsPerThread = kCols / kHalves;
+#ifndef TRI_TC_ACCS
+#define TRI_TC_ACCS 1
+#endif
+// accumulators per CTA: 2 = MMA b + 1 runs while the threads drain block b (ping-pong)
+constexpr int kAccs = TRI_TC_ACCS;
 #ifndef TRI_TC_CTAS
 #define TRI_TC_CTAS 4
 #endif
@@ -297,11 +308,11 @@ __device__ __forceinline__ void block_of(bool diag, int idx, int &rh, int &ch) {
 }
 
 template <int kRho, bool kBB>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kTileThreads, kCtasPerSm) collide_tc_kernel(TcArgs a) {
     constexpr int R = kRho / 128;
     constexpr uint32_t kOpBytes = kRho * 32;
     extern __shared__ __align__(1024) unsigned char dsm[];
-    __shared__ __align__(8) unsigned long long mbar[2];     // [0] operands landed, [1] MMA done
+    __shared__ __align__(8) unsigned long long mbar[1 + kAccs];   // [0] operands landed, [1 + a] MMA into acc a done
     __shared__ uint32_t taddr;
     uint32_t bi, bj;
     if (kBB) {                                         // m x m grid: blocks above the diagonal exit
@@ -318,10 +329,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs
     const int t = threadIdx.x, warp = t >> 5;
     const uint32_t xs = (uint32_t)__cvta_generic_to_shared(dsm), ys = xs + kOpBytes;
     const uint32_t mb_ld = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
-    const uint32_t mb_mma = (uint32_t)__cvta_generic_to_shared(&mbar[1]);
+    const uint32_t mb_mma = (uint32_t)__cvta_generic_to_shared(&mbar[1]);   // + 8 acc
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_ld));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_mma));
+#pragma unroll
+        for (int q = 0; q < kAccs; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_mma + 8 * q));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // the tile's operand rows: two contiguous runs of the workspace -> shared memory
         const uint16_t *gx = a.ops + (int64_t)bi * kRho * 16, *gy = a.ops + (a.npad + (int64_t)bj * kRho) * 16;
@@ -339,56 +351,63 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) collide_tc_kernel(TcArgs
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&taddr)),
-                     "n"(kCols));
+                     "n"(kCols * kAccs));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = taddr;
-    const uint32_t lanes = tmem + ((uint32_t)(warp * 32) << 16);
+    const int row = t & 127, colbase = (warp >> 2) * kColsPerThread;   // accumulator lane, first column
+    const uint32_t lanes = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)colbase;
     const bool diag = bi == bj;
     const int nblk = diag ? R * (R + 1) / 2 : R * R;
     auto issue = [&](int idx) {
         int rh, ch;
         block_of<R>(diag, idx, rh, ch);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        mma_f16(tmem, smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_mma)
+        const int acc = kAccs == 1 ? 0 : (idx & 1);
+        mma_f16(tmem + (uint32_t)(acc * kCols), smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         mb_mma + 8 * acc)
                      : "memory");
     };
     if (t == 0) {
         mbar_wait(mb_ld, 0, a.count);
         issue(0);
+        if (kAccs == 2 && nblk > 1) issue(1);
     }
     uint32_t cnt = 0;
 #pragma unroll 1
     for (int idx = 0; idx < nblk; ++idx) {
-        mbar_wait(mb_mma, (uint32_t)idx & 1u, a.count);
+        const int acc = kAccs == 1 ? 0 : (idx & 1);
+        mbar_wait(mb_mma + 8 * acc, (uint32_t)(kAccs == 1 ? idx : idx >> 1) & 1u, a.count);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        uint32_t v[4][16];
+        constexpr int NG = kColsPerThread / 32;            // 32-column groups per thread
+        uint32_t v[NG][16];
 #pragma unroll
-        for (int cg = 0; cg < 4; ++cg) ldtm16p(lanes + (uint32_t)(cg * 32), v[cg]);
+        for (int cg = 0; cg < NG; ++cg) ldtm16p(lanes + (uint32_t)(acc * kCols + cg * 32), v[cg]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         // the accumulator is in registers: hand it back, the next MMA runs during the tests
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
-        if (t == 0 && idx + 1 < nblk) issue(idx + 1);
-        const uint32_t o0 = or16(v[0]), o1 = or16(v[1]), o2 = or16(v[2]), o3 = or16(v[3]);
-        if ((or3(o0, o1, o2) | o3) & 0x80008000u) {          // rare: some value of the row is negative
+        if (t == 0 && idx + kAccs < nblk) issue(idx + kAccs);
+        uint32_t o[NG], any = 0;
+#pragma unroll
+        for (int cg = 0; cg < NG; ++cg) { o[cg] = or16(v[cg]); any |= o[cg]; }
+        if (any & 0x80008000u) {                           // rare: some value of the row is negative
             int rh, ch;
             block_of<R>(diag, idx, rh, ch);
-            const int64_t i = (int64_t)bi * kRho + rh * 128 + t;
-            const int64_t j0 = (int64_t)bj * kRho + ch * 128;
-            const int jlim = (diag && ch == rh) ? t : 128;   // strict j < i inside a diagonal block
-            if (o0 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[0]), i, j0, jlim);
-            if (o1 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[1]), i, j0 + 32, jlim - 32);
-            if (o2 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[2]), i, j0 + 64, jlim - 64);
-            if (o3 & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[3]), i, j0 + 96, jlim - 96);
+            const int64_t i = (int64_t)bi * kRho + rh * 128 + row;
+            const int64_t j0 = (int64_t)bj * kRho + ch * 128 + colbase;
+            const int jlim = ((diag && ch == rh) ? row : 128) - colbase;   // strict j < i inside a diagonal block
+#pragma unroll
+            for (int cg = 0; cg < NG; ++cg)
+                if (o[cg] & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[cg]), i, j0 + 32 * cg, jlim - 32 * cg);
         }
     }
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols * kAccs));
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((t & 31) == 0 && cnt) atomicAdd(a.count, (unsigned long long)cnt);
 }
@@ -515,8 +534,8 @@ static void launch_rho(const tri_map_t &m, TcArgs a, cudaStream_t st) {
     const int smem = 2 * kRho * 32 > pad ? 2 * kRho * 32 : pad;
     auto k = collide_tc_kernel<kRho, kBB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), kThreads, smem, st>>>(a);
-    else k<<<tile_grid(a.omega_end - a.omega_begin), kThreads, smem, st>>>(a);
+    if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), kTileThreads, smem, st>>>(a);
+    else k<<<tile_grid(a.omega_end - a.omega_begin), kTileThreads, smem, st>>>(a);
 }
 
 tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph, unsigned long long *count,
