@@ -13,13 +13,15 @@ cap edm edm_kernel edm --rho 128 --strategy lambda
 cap edm_bb edm_kernel edm --rho 128 --strategy bb
 cap collide collide_kernel collide --rho 256 --strategy lambda
 cap collide_bb collide_kernel collide --rho 256 --strategy bb
-cap collide_tc collide_tc_kernel collide --rho 1024 --strategy tc
-cap collide_tc_bb collide_tc_kernel collide --rho 1024 --strategy bb_tc
+cap collide_tc collide_tc_kernel collide --rho 768 --strategy tc
+cap collide_tc_bb collide_tc_kernel collide --rho 768 --strategy bb_tc
 cap collide1d collide1d_kernel collide1d --strategy lambda
 cap collide1d_bb collide1d_kernel collide1d --strategy bb
 cap ca ca_multi_kernel ca --rho 128 --strategy lambda
 cap ca_multi ca_multi_kernel ca_steps --rho 224 --k 8 --strategy lambda
 cap ca_multi_bb ca_multi_kernel ca_steps --rho 224 --k 8 --strategy bb
+cap ca_packed ca_packed_kernel ca_run --rho 240 --k 8 --strategy lambda
+cap ca_packed_bb ca_packed_kernel ca_run --rho 240 --k 8 --strategy bb
 cap triplet triplet32_kernel triplet --rho 32 --strategy lambda
 cap triplet_bb triplet32_kernel triplet --rho 32 --strategy bb
 cap dummy dummy_kernel dummy --rho 16 --strategy lambda
@@ -30,5 +32,5 @@ ls -la gpurun_out
 mkdir -p gpurun_out/prof && cp profiles/ncu_summary.json gpurun_out/prof/ 2>/dev/null
 TRI_PROF_DIR=gpurun_out/prof python tools/make_profiles.py "${TAG:-r02}" gpurun_out/launches.csv \
     $(for f in gpurun_out/*.ncu-rep; do b=$(basename $f .ncu-rep); echo "$b=$f"; done) > gpurun_out/prof/make.log 2>&1
-for f in gpurun_out/*.ncu-rep; do case $(basename $f) in edm.ncu-rep|collide_tc.ncu-rep) ;; *) rm -f $f ;; esac; done
+for f in gpurun_out/*.ncu-rep; do case $(basename $f) in edm.ncu-rep|collide_tc.ncu-rep|ca_packed.ncu-rep) ;; *) rm -f $f ;; esac; done
 du -sh gpurun_out
