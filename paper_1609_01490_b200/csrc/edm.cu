@@ -181,9 +181,9 @@ template <int DIM> struct LineSmem { static constexpr int FLOATS = 4 * DIM * kLi
 // the line phase (T(r0 + y) = T(r0) + r0 y + T(y) with r0 = 0 mod 128, and T(y) mod 32 is
 // the same on exactly these four y < 128), so one set of column loads serves 16 cells per
 // lane.  FULL: all four rows inside the domain, else bit g of vmask says row g is.
-template <int DIM, bool FULL>
-__device__ __forceinline__ void edm_line_quad(const float *rl, const float4 *rowp, int x, float *const (&pr)[4],
-                                              uint32_t s32, int vmask) {
+template <int DIM, bool FULL, class Addr>
+__device__ __forceinline__ void edm_line_quad(const float *rl, const float4 *rowp, int x, uint32_t s32, int vmask,
+                                              const Addr &addr) {
     const int delta = (int)((0u - s32) & 31u);
     const float *src = rl + (delta & 3) * DIM * kLineCols + (delta & ~3);
     ulonglong2 w[DIM];
@@ -213,7 +213,7 @@ __device__ __forceinline__ void edm_line_quad(const float *rl, const float4 *row
         float v[4];
         asm("mov.b64 {%0, %1}, %2;" : "=f"(v[0]), "=f"(v[1]) : "l"(a01));
         asm("mov.b64 {%0, %1}, %2;" : "=f"(v[2]), "=f"(v[3]) : "l"(a23));
-        st_cs_v4(pr[g] + delta, sqrt_approx(v[0]), sqrt_approx(v[1]), sqrt_approx(v[2]), sqrt_approx(v[3]));
+        st_cs_v4(addr(g, delta), sqrt_approx(v[0]), sqrt_approx(v[1]), sqrt_approx(v[2]), sqrt_approx(v[3]));
     }
 }
 
@@ -257,30 +257,63 @@ __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t
     __syncthreads();
     // warp w takes x = 4w .. 4w + 3: rows {x, 63 - x, 64 + x, 127 - x}, all 128 rows over 8 warps
     const int x0 = 4 * warp;
-    const int64_t rr0[4] = {r0 + x0, r0 + 63 - x0, r0 + 64 + x0, r0 + 127 - x0};
-    float *pr[4];
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-        pr[g] = a.out + (tri::T2((uint64_t)rr0[g]) + (uint64_t)c0 - a.out_offset) + 4 * lane;
-    uint32_t s32 = (uint32_t)(tri::T2((uint64_t)rr0[0]) + (uint64_t)c0 - a.out_offset);   // phase bits
     const float *rl = rot + 4 * lane;
     const bool full = r0 + 127 < a.n;
     const uint32_t u0 = (uint32_t)r0;
+    const uint64_t s0 = tri::T2((uint64_t)r0) + (uint64_t)c0 - a.out_offset;   // local start of row r0
+    auto vmask_of = [&](int x) {
+        return (int)(r0 + x < a.n) | ((int)(r0 + 63 - x < a.n) << 1) | ((int)(r0 + 64 + x < a.n) << 2) |
+               ((int)(r0 + 127 - x < a.n) << 3);
+    };
+    if (r0 < (int64_t)(1 << 25)) {
+        // rows r0 + y at 32-bit offsets T(r0 + y) - T(r0) = r0 y + T(y) < 2^32 from one 64-bit base:
+        // one IMAD.WIDE per store address, one IADD3 per row step
+        float *const B = a.out + s0 + 4 * lane;
+        const int ys[4] = {x0, 63 - x0, 64 + x0, 127 - x0};
+        uint32_t o[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        const int x = x0 + t;
+        for (int g = 0; g < 4; ++g) o[g] = u0 * (uint32_t)ys[g] + (uint32_t)(ys[g] * (ys[g] + 1) / 2);
+        const uint32_t sp = (uint32_t)s0;
+        auto addr = [&](int g, int delta) { return (B + delta) + o[g]; };
+        auto step = [&](int x) {
+            o[0] += u0 + (uint32_t)x + 1u;                // T(i + 1) - T(i) = i + 1
+            o[1] -= u0 + 63u - (uint32_t)x;               // T(i - 1) - T(i) = -i
+            o[2] += u0 + 65u + (uint32_t)x;
+            o[3] -= u0 + 127u - (uint32_t)x;
+        };
         if (full) {
-            edm_line_quad<DIM, true>(rl, rowp, x, pr, s32, 15);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                edm_line_quad<DIM, true>(rl, rowp, x0 + t, sp + o[0], 15, addr);
+                step(x0 + t);
+            }
         } else {
-            const int vmask = (r0 + x < a.n) | ((r0 + 63 - x < a.n) << 1) | ((r0 + 64 + x < a.n) << 2) |
-                              ((r0 + 127 - x < a.n) << 3);
-            if (vmask) edm_line_quad<DIM, false>(rl, rowp, x, pr, s32, vmask);
+#pragma unroll 1
+            for (int t = 0; t < 4; ++t) {
+                const int vmask = vmask_of(x0 + t);
+                if (vmask) edm_line_quad<DIM, false>(rl, rowp, x0 + t, sp + o[0], vmask, addr);
+                step(x0 + t);
+            }
         }
-        pr[0] += u0 + (uint32_t)x + 1u;                   // T(i + 1) - T(i) = i + 1
-        pr[1] -= u0 + 63u - (uint32_t)x;                  // T(i - 1) - T(i) = -i
-        pr[2] += u0 + 65u + (uint32_t)x;
-        pr[3] -= u0 + 127u - (uint32_t)x;
-        s32 += u0 + (uint32_t)x + 1u;
+    } else {                                              // very large n: 64-bit row pointers
+        const int64_t rr0[4] = {r0 + x0, r0 + 63 - x0, r0 + 64 + x0, r0 + 127 - x0};
+        float *pr[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+            pr[g] = a.out + (tri::T2((uint64_t)rr0[g]) + (uint64_t)c0 - a.out_offset) + 4 * lane;
+        uint32_t s32 = (uint32_t)(tri::T2((uint64_t)rr0[0]) + (uint64_t)c0 - a.out_offset);   // phase bits
+        auto addr = [&](int g, int delta) { return pr[g] + delta; };
+#pragma unroll 1
+        for (int t = 0; t < 4; ++t) {
+            const int x = x0 + t;
+            const int vmask = vmask_of(x);
+            if (vmask) edm_line_quad<DIM, false>(rl, rowp, x, s32, vmask, addr);
+            pr[0] += u0 + (uint32_t)x + 1u;
+            pr[1] -= u0 + 63u - (uint32_t)x;
+            pr[2] += u0 + 65u + (uint32_t)x;
+            pr[3] -= u0 + 127u - (uint32_t)x;
+            s32 += u0 + (uint32_t)x + 1u;
+        }
     }
 }
 
