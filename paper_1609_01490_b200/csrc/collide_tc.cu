@@ -38,13 +38,14 @@
 // ONE contiguous rho x 32-byte run each, staged into shared memory by two 1-D bulk copies
 // (cp.async.bulk, the TMA engine) completing on an mbarrier.
 //
-// CTA = 256 threads per tile (the paper's one block per lambda tile, Eq. 4, or the BB grid,
-// P:411-418), 128 TMEM columns.  Per 128 x 128 block one MMA (issued by one thread)
-// commits to an mbarrier; threads t and t + 128 = accumulator lane t & 127 = row t & 127 of
-// the block load one half of its 128 columns each (2 x tcgen05.ld.32x32b.x16.pack::16b: two
-// F16 values per register, 32 registers), the CTA hands the accumulator back (one barrier)
-// and thread 0 issues the next block's MMA while every thread ORs its 32 registers (16
-// three-input LOP3s: a quarter of an ALU op per pair) and tests bits 15 and 31.  A flagged (row, 32-column)
+// CTA = 256 sign-test threads + one issuer warp per tile (the paper's one block per lambda
+// tile, Eq. 4, or the BB grid), 128 TMEM columns.  Per 128 x 128 block one MMA
+// (issued by the issuer warp's lane 0) commits to an mbarrier; test threads t and t + 128 =
+// accumulator lane t & 127 = row t & 127 of the block load one half of its 128 columns each
+// (2 x tcgen05.ld.32x32b.x16.pack::16b: two F16 values per register, 32 registers), the CTA
+// hands the accumulator back (one barrier) and the issuer issues the next block's MMA while
+// every test thread ORs its 32 registers (16 three-input LOP3s: a quarter of an ALU op per
+// pair) and tests bits 15 and 31.  A flagged (row, 32-column)
 // group recounts only its negative columns with the exact predicate.  Diagonal tiles skip
 // the blocks above the diagonal and recount j < i only.  (Round 2 history in DESIGN.md:
 // the single-pass TF32 filter with F32 accumulators this replaces, persistent
@@ -55,21 +56,40 @@
 namespace {
 
 constexpr int kThreads = 128, kCols = 128;            // probes: one thread per accumulator lane
-#ifndef TRI_TC_HALVES
-#define TRI_TC_HALVES 2
+#ifndef TRI_TC_ISSUER
+#define TRI_TC_ISSUER 1
 #endif
-// tile kernel: warps w and w + 4 (w < 4) read TMEM lane quarter w; with TRI_TC_HALVES = 2 each
-// takes half of the 128 accumulator columns (8 warps per CTA, half the sign-test work each)
-constexpr int kHalves = TRI_TC_HALVES, kTileThreads = 128 * kHalves, kColsPerThread = kCols / kHalves;
+// TRI_TC_ISSUER: one extra warp only issues the MMAs.  tcgen05.mma blocks the issuing thread
+// until the tensor pipe accepts it (~250 clk behind the co-resident CTAs' MMAs, measured by
+// clock64 tracing); in a sign-testing warp that delay lands on the CTA's critical path.
+constexpr int kIssuer = TRI_TC_ISSUER;
 #ifndef TRI_TC_ACCS
 #define TRI_TC_ACCS 1
 #endif
 // accumulators per CTA: 2 = MMA b + 1 runs while the threads drain block b (ping-pong)
 constexpr int kAccs = TRI_TC_ACCS;
-#ifndef TRI_TC_CTAS
-#define TRI_TC_CTAS 4
+#ifndef TRI_TC_N
+#define TRI_TC_N 128
 #endif
-constexpr int kCtasPerSm = TRI_TC_CTAS;
+// Tile geometry: blocks of 128 rows x N columns, one tcgen05.mma (M = 128, N, K = 16) and one
+// commit each (N = TRI_TC_N when it divides the tile edge, else 128).  Sign-test threads: warp w
+// reads TMEM lane quarter w % 4 and the 64-column group w / 4, so 2 N test threads; TMEM
+// N x kAccs columns per CTA, at most 512 per SM, which caps the CTAs per SM.
+template <int kRho> struct TcCfg {
+    static constexpr int N = (kRho % TRI_TC_N == 0) ? TRI_TC_N : 128;
+    static constexpr int R = kRho / 128, CB = kRho / N;           // row / column blocks per tile
+    static constexpr int TEST = 2 * N, THREADS = TEST + 32 * kIssuer;
+    static constexpr int CTAS = 512 / (N * kAccs) < 8 ? 512 / (N * kAccs) : 8;
+    // kind::f16: F16 accumulator (D format 0), F16 A and B (formats 0), K-major, M = 128, N
+    static constexpr uint32_t IDESC = ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    static constexpr int diag_blocks() {                          // blocks of a diagonal tile
+        int s = 0;
+        for (int r = 0; r < R; ++r) s += (r * 128 + 127) / N + 1;
+        return s;
+    }
+};
+constexpr int kColsPerThread = 64;
+static_assert(TRI_TC_N == 64 || TRI_TC_N == 128 || TRI_TC_N == 256, "MMA N");
 constexpr double kKappaU = 1.0 / 65536.0;               // 2^-16 (relative margin)
 constexpr double kKappaA = 1.0 / 16777216.0;            // 2^-24 (absolute margin, scaled units)
 constexpr float kS = 32768.0f;                          // S = 2^15: the column operand's scale
@@ -197,11 +217,11 @@ constexpr uint32_t kIdescF16 = ((uint32_t)(kCols >> 3) << 17) | ((uint32_t)(128 
 constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCols >> 3) << 17) |
                                 ((uint32_t)(128 >> 4) << 24);
 
-__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc = kIdescF16) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}\n" ::"r"(tmem),
-        "l"(da), "l"(db), "r"(0), "r"(kIdescF16));
+        "l"(da), "l"(db), "r"(0), "r"(idesc));
 }
 
 __device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db) {
@@ -294,22 +314,34 @@ __device__ __noinline__ uint32_t recount(const float4 *sph, int64_t n, uint32_t 
     return cnt;
 }
 
-template <int R>
+// block index -> (row block rh, column block ch); a diagonal tile has only the blocks that
+// reach the lower triangle (ch N <= 128 rh + 127)
+template <class C>
 __device__ __forceinline__ void block_of(bool diag, int idx, int &rh, int &ch) {
-    if (diag) {                                        // triangular block index -> (rh, ch), ch <= rh
+    if (diag) {
         rh = 0;
+        int base = 0;
+        bool done = false;
 #pragma unroll
-        for (int r = 1; r < R; ++r) rh += idx >= r * (r + 1) / 2;
-        ch = idx - rh * (rh + 1) / 2;
+        for (int r = 0; r < C::R; ++r) {
+            const int c = (r * 128 + 127) / C::N + 1;
+            if (!done && idx >= base + c) {
+                base += c;
+                rh = r + 1;
+            } else {
+                done = true;
+            }
+        }
+        ch = idx - base;
     } else {
-        rh = idx / R;
-        ch = idx - rh * R;
+        rh = idx / C::CB;
+        ch = idx - rh * C::CB;
     }
 }
 
 template <int kRho, bool kBB>
-__global__ void __launch_bounds__(kTileThreads, kCtasPerSm) collide_tc_kernel(TcArgs a) {
-    constexpr int R = kRho / 128;
+__global__ void __launch_bounds__(TcCfg<kRho>::THREADS, TcCfg<kRho>::CTAS) collide_tc_kernel(TcArgs a) {
+    using C = TcCfg<kRho>;
     constexpr uint32_t kOpBytes = kRho * 32;
     extern __shared__ __align__(1024) unsigned char dsm[];
     __shared__ __align__(8) unsigned long long mbar[1 + kAccs];   // [0] operands landed, [1 + a] MMA into acc a done
@@ -327,10 +359,12 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) collide_tc_kernel(Tc
         tri::lambda_map(w, bi, bj);
     }
     const int t = threadIdx.x, warp = t >> 5;
+    constexpr int kIssueT = kIssuer ? C::TEST : 0;           // the thread that issues copies and MMAs
+    const bool issuer_warp = kIssuer && t >= C::TEST;
     const uint32_t xs = (uint32_t)__cvta_generic_to_shared(dsm), ys = xs + kOpBytes;
     const uint32_t mb_ld = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
     const uint32_t mb_mma = (uint32_t)__cvta_generic_to_shared(&mbar[1]);   // + 8 acc
-    if (t == 0) {
+    if (t == kIssueT) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_ld));
 #pragma unroll
         for (int q = 0; q < kAccs; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_mma + 8 * q));
@@ -351,7 +385,7 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) collide_tc_kernel(Tc
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&taddr)),
-                     "n"(kCols * kAccs));
+                     "n"(C::N * kAccs));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -361,23 +395,31 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) collide_tc_kernel(Tc
     const int row = t & 127, colbase = (warp >> 2) * kColsPerThread;   // accumulator lane, first column
     const uint32_t lanes = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)colbase;
     const bool diag = bi == bj;
-    const int nblk = diag ? R * (R + 1) / 2 : R * R;
+    const int nblk = diag ? C::diag_blocks() : C::R * C::CB;
     auto issue = [&](int idx) {
         int rh, ch;
-        block_of<R>(diag, idx, rh, ch);
+        block_of<C>(diag, idx, rh, ch);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int acc = kAccs == 1 ? 0 : (idx & 1);
-        mma_f16(tmem + (uint32_t)(acc * kCols), smem_desc(xs + rh * 4096), smem_desc(ys + ch * 4096));
+        mma_f16(tmem + (uint32_t)(acc * C::N), smem_desc(xs + rh * 4096), smem_desc(ys + ch * C::N * 32), C::IDESC);
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          mb_mma + 8 * acc)
                      : "memory");
     };
-    if (t == 0) {
+    if (t == kIssueT) {
         mbar_wait(mb_ld, 0, a.count);
         issue(0);
         if (kAccs == 2 && nblk > 1) issue(1);
     }
     uint32_t cnt = 0;
+    if (issuer_warp) {
+        // the issuer warp: one hand-back barrier per block, then the next MMA
+#pragma unroll 1
+        for (int idx = 0; idx < nblk; ++idx) {
+            __syncthreads();
+            if (t == kIssueT && idx + kAccs < nblk) issue(idx + kAccs);
+        }
+    } else {
 #pragma unroll 1
     for (int idx = 0; idx < nblk; ++idx) {
         const int acc = kAccs == 1 ? 0 : (idx & 1);
@@ -386,28 +428,30 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) collide_tc_kernel(Tc
         constexpr int NG = kColsPerThread / 32;            // 32-column groups per thread
         uint32_t v[NG][16];
 #pragma unroll
-        for (int cg = 0; cg < NG; ++cg) ldtm16p(lanes + (uint32_t)(acc * kCols + cg * 32), v[cg]);
+        for (int cg = 0; cg < NG; ++cg) ldtm16p(lanes + (uint32_t)(acc * C::N + cg * 32), v[cg]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         // the accumulator is in registers: hand it back, the next MMA runs during the tests
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
-        if (t == 0 && idx + kAccs < nblk) issue(idx + kAccs);
+        if (!kIssuer && t == 0 && idx + kAccs < nblk) issue(idx + kAccs);
         uint32_t o[NG], any = 0;
 #pragma unroll
         for (int cg = 0; cg < NG; ++cg) { o[cg] = or16(v[cg]); any |= o[cg]; }
         if (any & 0x80008000u) {                           // rare: some value of the row is negative
             int rh, ch;
-            block_of<R>(diag, idx, rh, ch);
+            block_of<C>(diag, idx, rh, ch);
             const int64_t i = (int64_t)bi * kRho + rh * 128 + row;
-            const int64_t j0 = (int64_t)bj * kRho + ch * 128 + colbase;
-            const int jlim = ((diag && ch == rh) ? row : 128) - colbase;   // strict j < i inside a diagonal block
+            const int64_t j0 = (int64_t)bj * kRho + ch * C::N + colbase;
+            // strict j < i inside a diagonal tile: tile column ch N + colbase + e < tile row 128 rh + row
+            const int jlim = diag ? rh * 128 + row - (ch * C::N + colbase) : kColsPerThread;
 #pragma unroll
             for (int cg = 0; cg < NG; ++cg)
                 if (o[cg] & 0x80008000u) cnt += recount(a.sph, a.n, neg_mask16(v[cg]), i, j0 + 32 * cg, jlim - 32 * cg);
         }
     }
+    }
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols * kAccs));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::N * kAccs));
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((t & 31) == 0 && cnt) atomicAdd(a.count, (unsigned long long)cnt);
 }
@@ -529,13 +573,14 @@ size_t collide_tc_ws_bytes(const tri_map_t &m) { return (size_t)kHdrBytes + (siz
 
 template <int kRho, bool kBB>
 static void launch_rho(const tri_map_t &m, TcArgs a, cudaStream_t st) {
-    // pad the dynamic smem so at most kCtasPerSm CTAs share an SM (their TMEM columns fit)
-    const int pad = 228 * 1024 / (kCtasPerSm + 1) + 1024;
+    using C = TcCfg<kRho>;
+    // pad the dynamic smem so at most C::CTAS CTAs share an SM (their TMEM columns fit)
+    const int pad = 228 * 1024 / (C::CTAS + 1) + 1024;
     const int smem = 2 * kRho * 32 > pad ? 2 * kRho * 32 : pad;
     auto k = collide_tc_kernel<kRho, kBB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), kTileThreads, smem, st>>>(a);
-    else k<<<tile_grid(a.omega_end - a.omega_begin), kTileThreads, smem, st>>>(a);
+    if (kBB) k<<<dim3((unsigned)m.m, (unsigned)m.m), C::THREADS, smem, st>>>(a);
+    else k<<<tile_grid(a.omega_end - a.omega_begin), C::THREADS, smem, st>>>(a);
 }
 
 tri_status launch_collide_tc(const tri_map_t &m, int strategy, const float *sph, unsigned long long *count,

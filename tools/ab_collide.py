@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--rho", type=int, default=768)
     ap.add_argument("--strategy", default="tc")
     ap.add_argument("--launches", type=int, default=10)
+    ap.add_argument("--nocheck", action="store_true", help="diagnostic builds: skip the count check")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     n = 200000
@@ -40,7 +41,7 @@ def main():
             tri._lib = L
             tri.tri_collide(m, a.strategy, s, cnt)
             torch.cuda.synchronize()
-            assert cnt.item() == 123650, (p, cnt.item())
+            assert a.nocheck or cnt.item() == 123650, (p, cnt.item())
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record()
             for _ in range(a.launches):
