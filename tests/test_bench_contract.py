@@ -40,6 +40,6 @@ def test_bench_line_edm():
     assert d["unit"] == "cells/s" and d["config"]["cells_per_step"] == 65536 * 65537 // 2
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= r.keys()
-    assert r["bound"] == "hbm" and 0 < r["frac"] < 1.2 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert r["bound"] == "hbm" and 0 < r["frac"] < 1.5 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     assert d["gpu_launches"] == 3                      # one edm_kernel launch per step
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
