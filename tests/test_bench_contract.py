@@ -43,3 +43,26 @@ def test_bench_line_edm():
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1.5 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     assert d["gpu_launches"] == 3                      # one edm_kernel launch per step
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_device():
+    """The N-rank bench path (omega-range split, count / energy all-reduce, CA halo exchange,
+    fused P2P halo stores) run as 2 torchrun ranks on one GPU over gloo: one JSON line from
+    rank 0, n_gpus = 2, the halo exchange timed separately."""
+    env = dict(os.environ, TRI_BENCH_BACKEND="gloo", TRI_BENCH_ONE_DEVICE="1")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= d.keys() and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["parallelism"] == "omega-range x2"
+    ca = d["workloads"]["ca"]
+    assert ca["halo_exchange_ms"] > 0 and ca["compute_only_ms"] > 0 and ca["p2p_ms"] > 0
+    assert d["workloads"]["collide"]["tc_count"] == 123650
