@@ -19,7 +19,8 @@
 // four rotated SoA copies (one aligned LDS.128 per coordinate per lane at any phase),
 // row points as float4s, the tile's rows walked as 32 same-phase quads {x, 63-x, 64+x,
 // 127-x} so one set of column loads serves 16 cells per lane, two cells per
-// FADD2/FMUL2/FFMA2; 4 CTAs per SM.  Round 2 measured 1.39 -> 1.28 ms per step in the
+// FADD2/FMUL2/FFMA2; 8 CTAs of 4 warps per SM (in the power-capped sustained loop 2-3 %
+// faster than 4 CTAs of 8 warps, 4 % slower per isolated launch).  Round 2 measured 1.39 -> 1.28 ms per step in the
 // bench's sustained loop (n = 65536, 3-D) and 1.55 -> 1.27 ms for 4 features.  In that loop
 // the board sits at its 1 kW power cap (SM clock ~1.6 GHz, sw_power_cap): the stores alone
 // cost 0.84 J per launch (= torch fill_), the arithmetic ~0.3 J more
@@ -52,6 +53,18 @@ struct EdmArgs {
 
 constexpr int kEdmThreads = 256;
 constexpr int kWarps = kEdmThreads / 32;
+#ifndef TRI_EDM128_NT
+#define TRI_EDM128_NT 128
+#endif
+#ifndef TRI_EDM128_CTAS
+#define TRI_EDM128_CTAS 8
+#endif
+// CTA shape per tile edge: rho = 128 (the line-owned path) TRI_EDM128_NT threads, at most
+// TRI_EDM128_CTAS CTAs per SM (register budget); the other edges 256 threads
+template <int RHO> struct EdmT {
+    static constexpr int NT = RHO == 128 ? TRI_EDM128_NT : kEdmThreads;
+    static constexpr int CTAS = RHO == 128 ? TRI_EDM128_CTAS : 4;
+};
 
 // Chunk width (floats) per tile edge: rho = 256 uses 32-byte chunks and the
 // sm_100 256-bit store (STG.E.ENL2.256, 1 KB per warp store), rho = 128 16-byte
@@ -231,7 +244,7 @@ __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t
     float4 *rowp = reinterpret_cast<float4 *>(rot + 4 * DIM * kLineCols);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __syncthreads();                                          // the previous tile's readers are done
-    for (int t = threadIdx.x; t < kLineCols + 3 + RHO; t += kEdmThreads) {
+    for (int t = threadIdx.x; t < kLineCols + 3 + RHO; t += EdmT<RHO>::NT) {
         const bool is_col = t < kLineCols + 3;
         const int64_t pt = is_col ? c0 + t : r0 + (t - kLineCols - 3);   // col <= c0 + 162 < r0
         if (!is_col && pt >= a.n) continue;
@@ -255,8 +268,10 @@ __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t
         }
     }
     __syncthreads();
-    // warp w takes x = 4w .. 4w + 3: rows {x, 63 - x, 64 + x, 127 - x}, all 128 rows over 8 warps
-    const int x0 = 4 * warp;
+    // warp w takes x = XW w .. XW w + XW - 1 (XW = 32 / warps): rows {x, 63 - x, 64 + x, 127 - x},
+    // all 128 rows over the CTA's warps
+    constexpr int XW = 32 / (EdmT<128>::NT / 32);
+    const int x0 = XW * warp;
     const float *rl = rot + 4 * lane;
     const bool full = r0 + 127 < a.n;
     const uint32_t u0 = (uint32_t)r0;
@@ -283,13 +298,13 @@ __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t
         };
         if (full) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < XW; ++t) {
                 edm_line_quad<DIM, true>(rl, rowp, x0 + t, sp + o[0], 15, addr);
                 step(x0 + t);
             }
         } else {
 #pragma unroll 1
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < XW; ++t) {
                 const int vmask = vmask_of(x0 + t);
                 if (vmask) edm_line_quad<DIM, false>(rl, rowp, x0 + t, sp + o[0], vmask, addr);
                 step(x0 + t);
@@ -304,7 +319,7 @@ __device__ __forceinline__ void edm_tile_interior_line(const EdmArgs &a, int64_t
         uint32_t s32 = (uint32_t)(tri::T2((uint64_t)rr0[0]) + (uint64_t)c0 - a.out_offset);   // phase bits
         auto addr = [&](int g, int delta) { return pr[g] + delta; };
 #pragma unroll 1
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < XW; ++t) {
             const int x = x0 + t;
             const int vmask = vmask_of(x);
             if (vmask) edm_line_quad<DIM, false>(rl, rowp, x, s32, vmask, addr);
@@ -327,7 +342,7 @@ __device__ __forceinline__ void edm_tile_checked(const EdmArgs &a, int64_t r0, i
     constexpr int L = RHO / CW;                       // chunk slots per row segment
     const int t = threadIdx.x;
 #pragma unroll 1
-    for (int q = t; q < RHO * L; q += kEdmThreads) {
+    for (int q = t; q < RHO * L; q += EdmT<RHO>::NT) {
         const int rr = q / L, k = q % L;
         const int64_t i = r0 + rr;
         if (i >= a.n) break;
@@ -377,7 +392,7 @@ __device__ __forceinline__ void edm_tile(const EdmArgs &a, uint32_t bi, uint32_t
 }
 
 template <int RHO, int DIM, int STRAT>
-__global__ void __launch_bounds__(kEdmThreads, 4) edm_kernel(EdmArgs a) {
+__global__ void __launch_bounds__(EdmT<RHO>::NT, EdmT<RHO>::CTAS) edm_kernel(EdmArgs a) {
     __shared__ __align__(16) float rot[OwnW<RHO>::OW == 32 ? LineSmem<DIM>::FLOATS : 4];
     if (STRAT == TRI_BB) {
         const uint32_t bj = blockIdx.x;
@@ -422,24 +437,24 @@ tri_status launch_rd(const tri_map_t &m, int strategy, EdmArgs a, cudaStream_t s
         if (tr1 <= tr0) return TRI_OK;
         if (tr1 - tr0 > 65535) return TRI_ENOTSUP;
         a.tile_row_begin = tr0;
-        edm_kernel<RHO, DIM, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), kEdmThreads, 0, st>>>(a);
+        edm_kernel<RHO, DIM, TRI_BB><<<dim3((unsigned)m.m, (unsigned)(tr1 - tr0)), EdmT<RHO>::NT, 0, st>>>(a);
     } else if (strategy == TRI_LAMBDA) {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
-        edm_kernel<RHO, DIM, TRI_LAMBDA><<<tri::tile_grid(nb), kEdmThreads, 0, st>>>(a);
+        edm_kernel<RHO, DIM, TRI_LAMBDA><<<tri::tile_grid(nb), EdmT<RHO>::NT, 0, st>>>(a);
     } else if (strategy == TRI_LAMBDA_CLC) {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
-        edm_kernel<RHO, DIM, TRI_LAMBDA_CLC><<<tri::tile_grid(nb), kEdmThreads, 0, st>>>(a);
+        edm_kernel<RHO, DIM, TRI_LAMBDA_CLC><<<tri::tile_grid(nb), EdmT<RHO>::NT, 0, st>>>(a);
     } else {
         const uint64_t nb = a.omega_end - a.omega_begin;
         if (!nb) return TRI_OK;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edm_kernel<RHO, DIM, TRI_LAMBDA_PERSIST>,
-                                                      kEdmThreads, 0);
+                                                      EdmT<RHO>::NT, 0);
         uint64_t g = (uint64_t)tri::sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
         if (g > nb) g = nb;
-        edm_kernel<RHO, DIM, TRI_LAMBDA_PERSIST><<<(unsigned)g, kEdmThreads, 0, st>>>(a);
+        edm_kernel<RHO, DIM, TRI_LAMBDA_PERSIST><<<(unsigned)g, EdmT<RHO>::NT, 0, st>>>(a);
     }
     tri::note_launches(1);
     return tri::cuda_status();
