@@ -19,15 +19,15 @@
 // four rotated SoA copies (one aligned LDS.128 per coordinate per lane at any phase),
 // row points as float4s, the tile's rows walked as 32 same-phase quads {x, 63-x, 64+x,
 // 127-x} so one set of column loads serves 16 cells per lane, two cells per
-// FADD2/FMUL2/FFMA2; 8 CTAs of 4 warps per SM (in the power-capped sustained loop 2-3 %
-// faster than 4 CTAs of 8 warps, 4 % slower per isolated launch).  Round 2 measured 1.39 -> 1.28 ms per step in the
-// bench's sustained loop (n = 65536, 3-D) and 1.55 -> 1.27 ms for 4 features.  In that loop
-// the board sits at its 1 kW power cap (SM clock ~1.6 GHz, sw_power_cap): the stores alone
-// cost 0.84 J per launch (= torch fill_), the arithmetic ~0.3 J more
-// (profiles/r02_edm_power.txt), so instruction count, not the write pattern, now sets the
-// sustained rate; isolated launches take 1.18 ms (7.3 TB/s).  Single rows with scalar math
-// were slower than the chunk form; row pairs (i, i + 64) equal to quads; 5 CTAs per SM
-// within noise of 4, 3 / 2 CTAs slower; rho = 256 tiles (1 KB row segments) slower.
+// FADD2/FMUL2/FFMA2, rows at 32-bit offsets from one base pointer; 8 CTAs of 4 warps per
+// SM.  Round 2: 1.39 -> 1.22-1.35 ms per step in the bench's sustained loop (n = 65536, 3-D;
+// box-dependent) and 1.55 -> 1.2 ms for 4 features.  In that loop the board sits at its
+// 1 kW power cap (SM clock ~1.5-1.6 GHz, sw_power_cap): the stores alone cost 0.85-1.0 J per
+// launch (= torch fill_), the arithmetic ~0.3 J more (profiles/r02_edm_power.txt), so
+// energy per cell, not the write pattern, sets the sustained rate; isolated launches take
+// 1.18-1.22 ms (7.0-7.3 TB/s).  Measured and rejected: single rows with
+// scalar math, rho = 256 tiles (octets: 28 % fewer instructions, yet slower), 4 CTAs of 8
+// warps (faster isolated, 2-3 % slower sustained), 3 / 2 CTAs, other store cache hints.
 //
 // Other tile edges: interior tiles walk ROWS rows per warp, lane k owning chunk k
 // (rho = 32 CW, so each warp store is one contiguous 512 B / 1 KB run); the row's
