@@ -172,7 +172,8 @@ tri_status tri_dummy(const tri_map_t *map, int32_t strategy, int32_t mode,
  * TRI_BB, TRI_LAMBDA_PERSIST, TRI_LAMBDA_CLC or TRI_RB (world = 1); world > 1
  * needs a snapped map (the rank's slice is contiguous).  Stores are aligned
  * 16-byte streaming stores; each 16-byte chunk of the slice is written by exactly
- * one thread. */
+ * one thread (at rho = 128 each 128-byte line of the slice by one warp store, so a
+ * 128-byte-aligned d_out gives whole-line writes). */
 tri_status tri_edm(const tri_map_t *map, int32_t strategy, const float *d_pts,
                    int32_t dim, int64_t ld, size_t pts_bytes, float *d_out, size_t out_bytes,
                    void *stream);
