@@ -75,6 +75,7 @@ class ClockSampler:
         self.dev = dev_index
         self.proc = None
         self.lines = []
+        self.win = None
 
     def start(self):
         try:
@@ -90,7 +91,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))      # arrival time ~ sample time
+
+    def window(self, t0, t1):
+        """Keep only the samples taken while the timed loop ran on the GPU."""
+        self.win = (t0, t1)
 
     def stop(self):
         if self.proc is None:
@@ -104,7 +109,12 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, pw, pwi, lim, reasons = [], [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for ts, ln in self.lines]
+        if self.win is not None:
+            inside = [ln for ts, ln in self.lines if self.win[0] <= ts <= self.win[1] + 0.06]
+            if len(inside) >= 2:
+                lines = inside
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -156,12 +166,16 @@ def time_steps(step, K, W, world, sampler_dev=None):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier(world)
+    t0 = time.time()
     e0.record(s)
     for _ in range(K):
         step()
     e1.record(s)
     torch.cuda.synchronize()
+    t1 = time.time()
     barrier(world)
+    if clk is not None:
+        clk.window(t0, t1)
     clocks = clk.stop() if clk is not None else None
     return e0.elapsed_time(e1), clocks
 
