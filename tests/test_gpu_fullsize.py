@@ -149,3 +149,34 @@ def test_edm_host_bench_config(orc):
         ref = orc.edm(pts_h, r, r + 1)
         got = out[T(r):T(r) + r + 1]
         assert np.all(np.abs(got - ref) <= np.maximum(1e-5 * np.abs(ref), 1e-6)), r
+
+
+@pytest.mark.parametrize("strategy", ["lambda", "bb"])
+def test_edm_tile_row_past_2_25(orc, strategy):
+    """One tile row of an n = 2^25 + 1000 EDM (rows [r0, r0 + 128), r0 = 262145 * 128 > 2^25,
+    each row ~33.5 M cells; 17.2 GB of output): the line-owned interior tiles' 64-bit row
+    pointer path (taken only for r0 >= 2^25) and the diagonal tiles' checked path at 64-bit
+    offsets.  The map is the snapped slice of that tile row (row and omega range set by hand);
+    every cell is written and rows covering all four members of a same-phase quad, both walk
+    ends and the diagonal tile match the oracle."""
+    rho, bi = 128, 262145
+    n = (1 << 25) + 1000
+    r0 = bi * rho
+    assert r0 >= (1 << 25) and r0 + rho <= n
+    m = tri.tri_map_init(n, rho)
+    m.world, m.rank, m.snap = 2, 1, 1
+    m.row_begin, m.row_end = r0, r0 + rho
+    m.omega_begin, m.omega_end = T(bi), T(bi + 1)
+    m.out_offset, m.out_cells = T(r0), T(r0 + rho) - T(r0)
+    pts_h = inputs.points(n, 3, 7)
+    pts = torch.from_numpy(pts_h).cuda()
+    out = torch.full((m.out_cells,), float("nan"), dtype=torch.float32, device="cuda")
+    tri.tri_edm(m, strategy, pts, out)
+    torch.cuda.synchronize()
+    assert not torch.isnan(out).any().item()                       # every cell of the slice written
+    for y in (0, 1, 31, 32, 63, 64, 95, 96, 126, 127):            # quads {x, 63-x, 64+x, 127-x}
+        r = r0 + y
+        got = out[T(r) - m.out_offset:T(r) - m.out_offset + r + 1].cpu().numpy()
+        ref = orc.edm(pts_h, r, r + 1)
+        assert np.all(np.abs(got - ref) <= np.maximum(1e-5 * np.abs(ref), 1e-6)), y
+    del out
