@@ -24,6 +24,7 @@ def main():
     ap.add_argument("libs", nargs="+")
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--strategy", nargs="+", default=["lambda"])
     a = ap.parse_args()
     torch.cuda.set_device(0)
     n = 32768
@@ -33,25 +34,25 @@ def main():
     x = torch.from_numpy(inputs.ca_state(n, 42)).cuda()
     y = torch.empty_like(x)
     ws = torch.empty(tri.tri_ca_run_workspace_size(m), dtype=torch.uint8, device="cuda")
-    times = {p: [] for p in a.libs}
+    runs = [(p, L, st) for p, L in zip(a.libs, libs) for st in a.strategy]
+    times = {(p, st): [] for p, _, st in runs}
     ref = None
     for rep in range(a.reps + 1):
-        for p, L in zip(a.libs, libs):
+        for p, L, st in runs:
             tri._lib = L
-            tri.tri_ca_run(m, "lambda", a.steps, x, y, ws)
+            tri.tri_ca_run(m, st, a.steps, x, y, ws)
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record()
-            tri.tri_ca_run(m, "lambda", a.steps, x, y, ws)
+            tri.tri_ca_run(m, st, a.steps, x, y, ws)
             e1.record()
             torch.cuda.synchronize()
             if ref is None:
                 ref = y.clone()
             assert torch.equal(y, ref), f"{p}: result differs from {a.libs[0]}"
             if rep:
-                times[p].append(e0.elapsed_time(e1))
-    for p in a.libs:
-        t = times[p]
-        print(f"{p}: median {statistics.median(t):.4f} min {min(t):.4f} max {max(t):.4f} ms per {a.steps} generations")
+                times[(p, st)].append(e0.elapsed_time(e1))
+    for (p, st), t in times.items():
+        print(f"{p} {st}: median {statistics.median(t):.4f} min {min(t):.4f} max {max(t):.4f} ms per {a.steps} generations")
 
 
 if __name__ == "__main__":
